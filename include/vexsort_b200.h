@@ -1,0 +1,145 @@
+/*
+ * vexsort_b200.h -- C ABI of the B200-native hybrid sort.
+ *
+ * Drop-in boundary for the hot path of the reference package `vexsort`
+ * (arXiv 1704.08579).  The reference's plugin boundary is the numba kernel
+ * module pkg/src/vexsort/_kernels.py, called from quicksort.py,
+ * partition.py, smallsort.py and keyvalue.py whenever
+ * `backend.uses_kernels` (lanes.py:297).  Two families of entry points:
+ *
+ *  1. vx_host_* -- HOST-buffer twins of the _kernels.py functions, same
+ *     argument order and meaning, in-place on caller memory; the library
+ *     copies to the B200, runs the kernels and copies back.  These are what
+ *     a maintainer binds in place of `_kernels`.
+ *  2. vx_* device API -- device pointers, caller-provided workspace, an
+ *     explicit cudaStream_t, stream-ordered, no allocation; used by the
+ *     PyTorch-facing Python package and by bench.py.
+ *
+ * Element kinds (lanes.py:50-63, kind_of lanes.py:502-507): VX_I32 = int32
+ * keys, VX_F64 = float64 keys.  Key/value values must have the key's element
+ * width (keyvalue.py:44-47): 32-bit values with int32 keys, 64-bit values
+ * with float64 keys; their bits are moved, never interpreted.
+ *
+ * Every function returns 0 (or a non-negative index) on success and a
+ * negative VX_E* code on failure; vx_last_error() returns a thread-local
+ * message for the last failure.  NaN keys are unsupported, as in the
+ * reference (quicksort.py:140-141).
+ */
+#ifndef VEXSORT_B200_H
+#define VEXSORT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *vx_stream_t; /* == cudaStream_t */
+
+enum { VX_I32 = 0, VX_F64 = 1 };
+enum {
+    VX_OK = 0,
+    VX_EINVAL = -1,    /* bad argument (reference: AssertionError / ValueError) */
+    VX_ETYPE = -2,     /* unsupported dtype (reference: TypeError, lanes.py:507) */
+    VX_ECUDA = -3,     /* CUDA runtime / launch failure */
+    VX_EWORKSPACE = -4,/* workspace too small */
+    VX_ECAPACITY = -5, /* internal queue capacity exceeded */
+    VX_ETOOLONG = -6   /* a small-sort segment exceeds 256 elements */
+};
+
+/* SortConfig (quicksort.py:28-46).  sort_bound <= 0 selects the default
+ * 16*lanes (256 int32 / 128 float64); it is the largest range handed to the
+ * bitonic network and must be <= 16*lanes (quicksort.py:49-52).
+ * pivot_strategy (0 median3, 1 middle, 2 random) and the two partition flags
+ * are accepted for drop-in fidelity; the B200 driver samples its pivots
+ * (seeded by pivot_seed) and the flags do not apply to a GPU partition. */
+typedef struct {
+    int64_t sort_bound;
+    int32_t pivot_strategy;
+    int32_t skip_empty_stores;
+    int32_t swap_buffered;
+    int32_t reserved;
+    uint64_t pivot_seed;
+} vx_sort_config;
+
+const char *vx_last_error(void);
+int vx_version(void);
+
+/* ------------------------------------------------------------------ device API */
+
+/* Full hybrid sort, in place on device keys[n] (values[n] optional, may be
+ * NULL).  Replaces _kernels.quicksort / kv_quicksort (_kernels.py:378-482)
+ * as called by sort_with_config (quicksort.py:115-134) and kv_sort
+ * (keyvalue.py:228-252). */
+size_t vx_sort_workspace_bytes(int dtype, int has_values, int64_t n);
+int vx_sort(int dtype, void *keys, void *values, int64_t n, const vx_sort_config *cfg, void *ws,
+            size_t ws_bytes, vx_stream_t stream);
+
+/* Pivot partition, out of place: out[0:split) <= pivot < out[split:n).
+ * *pivot points to a HOST scalar of the key type.  The split (= count of
+ * keys <= pivot) is written to the DEVICE int64 *d_split.  Replaces
+ * _kernels.partition / kv_partition / scalar_partition (_kernels.py:162-262,
+ * 264-356) as called by partition_region (partition.py:115-145) and
+ * kv_partition_region (keyvalue.py:138-161). */
+size_t vx_partition_workspace_bytes(int dtype, int64_t n);
+int vx_partition(int dtype, const void *in_keys, const void *in_values, void *out_keys, void *out_values,
+                 int64_t n, const void *pivot, int64_t *d_split, void *ws, size_t ws_bytes,
+                 vx_stream_t stream);
+
+/* Batched small sort of CSR segments [offs[s], offs[s+1]) in place, every
+ * segment <= 256 elements (config 2).  Replaces one _kernels.smallsort_region
+ * call per segment (_kernels.py:115-126; sort_small_region,
+ * smallsort.py:218-252).  ws >= 4 bytes holds a device error flag that
+ * vx_segments_status() reads back (synchronising). */
+int vx_sort_segments(int dtype, void *keys, void *values, const int64_t *d_offsets, int64_t nseg, void *ws,
+                     size_t ws_bytes, vx_stream_t stream);
+int vx_segments_status(void *ws, vx_stream_t stream);
+
+/* Sharded sample sort building blocks (no reference counterpart; BASELINE
+ * config 5).  Splitters are (key, global index) pairs so equal keys are
+ * split by position.  Buckets: dest(x at global index g) = number of
+ * splitters lexicographically below (x, g).  out is grouped by destination;
+ * d_counts[nsplit+1] receives per-destination counts. */
+size_t vx_bucket_partition_workspace_bytes(int dtype, int nsplit);
+int vx_bucket_partition(int dtype, const void *in_keys, void *out_keys, int64_t n, uint64_t global_offset,
+                        const void *d_split_keys, const uint64_t *d_split_idx, int nsplit,
+                        unsigned long long *d_counts, void *ws, size_t ws_bytes, vx_stream_t stream);
+int vx_select_splitters(int dtype, const void *d_sample_keys, const uint64_t *d_sample_idx, int64_t count,
+                        int nparts, void *d_out_keys, uint64_t *d_out_idx, vx_stream_t stream);
+
+/* Seeded synthetic inputs generated on the device (bench only).
+ * dist: 0 uniform (int32 full range / f64 [-1e6,1e6)), 1 sorted, 2 reverse,
+ * 3 few-unique [0,16), 4 standard normal (f64), 5 uniform [0,2^31) int32,
+ * 6 index (values = global index). */
+int vx_generate(int dtype, int dist, void *out, int64_t n, uint64_t seed, uint64_t global_offset,
+                int64_t global_n, vx_stream_t stream);
+
+/* ------------------------------------------------------- host-buffer drop-in */
+/* Same argument order as the _kernels.py functions they replace.  Arrays are
+ * HOST memory (pinned or pageable), mutated in place; lo/hi are absolute.
+ * `lane` and `sentinel` are validated against the element kind and otherwise
+ * unused (the GPU has no 512-bit packs).  `pivot` points to a host scalar of
+ * the key type.  Partition functions return the absolute boundary. */
+int vx_host_quicksort(int dtype, void *arr, int64_t n, int64_t lane, int64_t sort_bound, int strategy,
+                      int opt_a, int opt_b, uint64_t seed);                      /* _kernels.py:378 */
+int vx_host_kv_quicksort(int dtype, void *keys, void *vals, int64_t n, int64_t lane, int64_t sort_bound,
+                         int strategy, int opt_a, int opt_b, uint64_t seed);     /* _kernels.py:425 */
+int64_t vx_host_partition(int dtype, void *arr, int64_t lo, int64_t hi, const void *pivot, int64_t lane,
+                          int opt_a, int opt_b);                                 /* _kernels.py:257 */
+int64_t vx_host_kv_partition(int dtype, void *keys, void *vals, int64_t lo, int64_t hi, const void *pivot,
+                             int64_t lane, int opt_a, int opt_b);                /* _kernels.py:347 */
+int64_t vx_host_scalar_partition(int dtype, void *arr, int64_t lo, int64_t hi, const void *pivot);
+                                                                                 /* _kernels.py:162 */
+int64_t vx_host_kv_scalar_partition(int dtype, void *keys, void *vals, int64_t lo, int64_t hi,
+                                    const void *pivot);                          /* _kernels.py:173 */
+int vx_host_smallsort_region(int dtype, void *arr, int64_t lo, int64_t length);  /* _kernels.py:115 */
+int vx_host_kv_smallsort_region(int dtype, void *keys, void *vals, int64_t lo, int64_t length);
+                                                                                 /* _kernels.py:148 */
+/* Free the device arena the host functions keep between calls. */
+int vx_host_release(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VEXSORT_B200_H */

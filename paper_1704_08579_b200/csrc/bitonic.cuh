@@ -1,0 +1,149 @@
+// bitonic.cuh -- warp-register bitonic sorting network (north-star subsystem 2).
+//
+// The network is the reference's same-direction bitonic network
+// (_kernels.py:30-58, smallsort.py:88-117): for every block size s a
+// *crossing* round compares slot i with slot (blk + s-1-k), i.e. partner
+// i ^ (s-1), then *linear* rounds of halving distance d compare i with
+// i ^ d.  Every comparator leaves the minimum at the lower index, so padding
+// with the sentinel (INT32_MAX / +inf) at the end cannot change the written
+// prefix (sentinel padding by count, _kernels.py:97-113).
+//
+// Key/value: a pair is swapped only on a strict key inversion (b < a),
+// exactly as _kv_net (_kernels.py:60-95), so equal keys keep their values.
+//
+// Layout: one warp holds P = 32*E slots, slot q = lane*E + r lives in
+// register r of `lane` (blocked).  Comparators whose XOR distance is < E are
+// in-register; larger distances cross lanes with __shfl_xor_sync (lane mask
+// = dist / E, register mask = dist % E).  Each side of a cross-lane pair
+// computes its own half from the *old* values, so all partner values are
+// gathered before any update.
+#pragma once
+
+#include "common.cuh"
+
+namespace vx {
+
+template <typename K, typename V, int E>
+struct WarpBitonic {
+    static constexpr int P = 32 * E;
+    static constexpr bool KV = HasVal<V>::value;
+
+    // one comparator round with XOR distance `mask` over all P slots
+    template <int MASK>
+    __device__ __forceinline__ static void round(K (&k)[E], V (&v)[E]) {
+        if constexpr (MASK < E) {
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int r2 = r ^ MASK;
+                if (r < r2) {
+                    // slot r is the lower index: minimum stays at r
+                    K a = k[r], b = k[r2];
+                    bool sw = b < a;  // strict inversion; equals (a<=b ? a : b) for keys
+                    k[r] = sw ? b : a;
+                    k[r2] = sw ? a : b;
+                    if constexpr (KV) {
+                        V x = v[r], y = v[r2];
+                        v[r] = sw ? y : x;
+                        v[r2] = sw ? x : y;
+                    }
+                }
+            }
+        } else {
+            constexpr int LM = MASK / E;   // lane xor mask
+            constexpr int RM = MASK % E;   // register xor mask (E-1 on crossing rounds, else 0)
+            constexpr int HB = 1 << (31 - __builtin_clz(LM));  // highest lane bit
+            const int lane = threadIdx.x & 31;
+            const bool low = (lane & HB) == 0;
+            K pk[E];
+            V pv[E];
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                pk[r] = __shfl_xor_sync(0xffffffffu, k[r ^ RM], LM);
+                if constexpr (KV) pv[r] = __shfl_xor_sync(0xffffffffu, v[r ^ RM], LM);
+            }
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                // low side takes the partner iff partner < mine; high side iff mine < partner
+                bool take = low ? (pk[r] < k[r]) : (k[r] < pk[r]);
+                k[r] = take ? pk[r] : k[r];
+                if constexpr (KV) v[r] = take ? pv[r] : v[r];
+            }
+        }
+    }
+
+    template <int S, int D>
+    __device__ __forceinline__ static void linear(K (&k)[E], V (&v)[E]) {
+        if constexpr (D >= 1) {
+            round<D>(k, v);
+            linear<S, D / 2>(k, v);
+        }
+    }
+
+    template <int S>
+    __device__ __forceinline__ static void stage(K (&k)[E], V (&v)[E]) {
+        if constexpr (S <= P) {
+            round<S - 1>(k, v);      // crossing round: partner i ^ (s-1)
+            linear<S, S / 4>(k, v);  // linear rounds d = s/4 .. 1
+            stage<S * 2>(k, v);
+        }
+    }
+
+    __device__ __forceinline__ static void sort(K (&k)[E], V (&v)[E]) { stage<2>(k, v); }
+};
+
+// Sort one region of `len` (<= 32*E) elements: load blocked with sentinel
+// padding by count, run the network, write back exactly `len` elements.
+// src and dst may alias (in-place) -- every lane reads all its slots before
+// any lane writes.
+template <typename K, typename V, int E>
+__device__ __forceinline__ void warp_sort_region(const K* src_k, const V* src_v, K* dst_k, V* dst_v,
+                                                 uint64_t start, uint32_t len) {
+    constexpr bool KV = HasVal<V>::value;
+    const int lane = threadIdx.x & 31;
+    K k[E];
+    V v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t q = lane * E + r;
+        k[r] = q < len ? src_k[start + q] : KeyTraits<K>::sentinel();
+        if constexpr (KV) v[r] = q < len ? src_v[start + q] : V();
+    }
+    __syncwarp();
+    WarpBitonic<K, V, E>::sort(k, v);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const uint32_t q = lane * E + r;
+        if (q < len) {
+            dst_k[start + q] = k[r];
+            if constexpr (KV) dst_v[start + q] = v[r];
+        }
+    }
+}
+
+// Dispatch on the padded size class (P = 32, 64, 128, 256).  Returns false
+// if len exceeds 256.
+template <typename K, typename V>
+__device__ __forceinline__ bool warp_sort_any(const K* src_k, const V* src_v, K* dst_k, V* dst_v,
+                                              uint64_t start, uint32_t len) {
+    if (len <= 32) {
+        warp_sort_region<K, V, 1>(src_k, src_v, dst_k, dst_v, start, len);
+    } else if (len <= 64) {
+        warp_sort_region<K, V, 2>(src_k, src_v, dst_k, dst_v, start, len);
+    } else if (len <= 128) {
+        warp_sort_region<K, V, 4>(src_k, src_v, dst_k, dst_v, start, len);
+    } else if (len <= 256) {
+        warp_sort_region<K, V, 8>(src_k, src_v, dst_k, dst_v, start, len);
+    } else {
+        return false;
+    }
+    return true;
+}
+
+// Pointer-offset form: sort src[0..len) into dst[0..len) (src may alias dst,
+// and may live in shared memory).
+template <typename K, typename V>
+__device__ __forceinline__ bool warp_sort_any2(const K* src_k, const V* src_v, K* dst_k, V* dst_v, uint32_t len) {
+    return warp_sort_any<K, V>(src_k, src_v, dst_k, dst_v, 0, len);
+}
+
+}  // namespace vx

@@ -1,0 +1,101 @@
+// common.cuh -- shared device helpers for the B200 hybrid sort (sm_100a).
+//
+// Element kinds follow the reference's ElemKind (lanes.py:50-63): int32 keys
+// with sentinel INT32_MAX, float64 keys with sentinel +inf.  Keys are compared
+// by VALUE (never by bit pattern), so -0.0 == +0.0 exactly as in the
+// reference's ordered-quiet compares.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vx {
+
+constexpr int kWarp = 32;
+
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<int32_t> {
+    __host__ __device__ static constexpr int32_t sentinel() { return 0x7fffffff; }
+};
+template <>
+struct KeyTraits<double> {
+    __host__ __device__ static constexpr double sentinel() { return __builtin_huge_val(); }
+};
+
+// "no payload" marker type for key-only instantiations
+struct NoVal {};
+template <typename V>
+struct HasVal { static constexpr bool value = true; };
+template <>
+struct HasVal<NoVal> { static constexpr bool value = false; };
+
+// ---------------------------------------------------------------- memory
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// streaming (read-once) loads: keep L1 clean, evict-first in L2
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T* p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------- scans
+// Inclusive warp scan of a 32-bit value.
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned t = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += t;
+    }
+    return v;
+}
+
+// Exclusive block scan of one 32-bit value per thread.  `smem` needs
+// NWARPS+1 words.  Returns the exclusive prefix; *total receives the sum.
+template <int NTHREADS>
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* smem, unsigned* total) {
+    constexpr int NW = NTHREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned inc = warp_incl_scan(v);
+    if (lane == 31) smem[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned w = lane < NW ? smem[lane] : 0u;
+        unsigned wi = warp_incl_scan(w);
+        if (lane < NW) smem[lane] = wi - w;
+        if (lane == NW - 1) smem[NW] = wi;
+    }
+    __syncthreads();
+    unsigned r = smem[warp] + inc - v;
+    *total = smem[NW];
+    __syncthreads();
+    return r;
+}
+
+// 64-bit hash (splitmix64 finaliser) for deterministic sample positions.
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+__host__ __device__ __forceinline__ uint32_t next_pow2_u32(uint32_t v) {
+    uint32_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace vx

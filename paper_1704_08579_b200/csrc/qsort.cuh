@@ -1,0 +1,752 @@
+// qsort.cuh -- device-side hybrid quicksort driver (north-star subsystem 3)
+// and the k-way bucket partition (subsystem 4's partition step).
+//
+// Reference algorithm: _kernels.quicksort (_kernels.py:378-423) -- pick a
+// pivot, partition, recurse on both sides, hand ranges <= sort_bound to the
+// bitonic small sort.  The GPU keeps that structure but partitions each
+// range around MANY sampled pivots at once (a multi-pivot quicksort / sample
+// sort step) so the number of HBM passes is ~log_256(n) instead of log_2(n):
+//
+//   level loop (work queue of segments in device memory, ping-pong buffers)
+//     qs_plan     one CTA per segment: sample, sort the sample in smem, pick
+//                 up to 255 distinct pivots (= splitters), allocate bucket /
+//                 tile slots with atomics
+//     qs_hist     persistent CTAs over the level's tiles: classify each
+//                 element into 2m+1 buckets (ranges + "equal to pivot"
+//                 buckets), per-segment histograms
+//     qs_emit     one CTA per segment: scan the histogram into bucket cursors
+//                 and enqueue children: big -> next level, <= LOCAL_MAX ->
+//                 finish queue, equal-to-pivot / singletons -> final
+//     qs_scatter  persistent CTAs over tiles: classify again, rank inside the
+//                 tile, reserve a run per bucket with one atomic, stage the
+//                 tile in smem bucket-major and write runs coalesced
+//     qs_finish   one CTA per finish item: CTA-local hybrid quicksort in
+//                 shared memory (one more sampled multi-pivot partition, then
+//                 the warp bitonic network on every range <= 256) straight
+//                 into the output; or a chunked copy for final buckets that
+//                 sit in the scratch buffer.
+//
+// The equal-to-pivot buckets are final (all keys equal), which removes the
+// reference's quadratic behaviour on few-unique / sorted / reverse inputs
+// (SURVEY.md section 0 finding 5) without changing the (unique) output.
+#pragma once
+
+#include "bitonic.cuh"
+#include "common.cuh"
+
+namespace vx {
+
+constexpr int kMaxSplit = 255;                 // pivots per segment (level)
+constexpr int kMaxBkt = 2 * kMaxSplit + 1;     // 511 buckets
+constexpr int kQsNT = 256;                     // tile-kernel threads
+constexpr int kPlanNT = 512;                   // plan / emit threads
+constexpr int kFinNT = 512;                    // finish-kernel threads
+constexpr int kMaxSample = 4096;
+constexpr int kFinSample = 1024;
+constexpr uint32_t kCopyChunk = 16384;
+constexpr int kMaxLevels = 48;
+
+template <typename K>
+struct QsTile { static constexpr int IPT = 16; };   // 4096 int32 / 4096 f64 per tile
+template <typename K>
+constexpr int qs_tile() { return kQsNT * QsTile<K>::IPT; }
+
+// Elements a finish CTA sorts in shared memory (keys + payload, x2 buffers).
+template <typename K, typename V>
+struct FinCap {
+    static constexpr uint32_t bytes_per = sizeof(K) + (HasVal<V>::value ? sizeof(V) : 0);
+    // power of two so the rare CTA-bitonic fallback (padded) always fits
+    static constexpr uint32_t value = bytes_per <= 4 ? 8192 : (bytes_per <= 8 ? 4096 : 2048);
+};
+
+struct Seg {
+    unsigned long long start, len;
+    unsigned spl_off, m, bkt_off, tile_base;
+};
+struct Fin {
+    unsigned long long start;
+    unsigned len, flags;  // bit0: source is the scratch buffer; bit1: copy only
+};
+struct Ctl {
+    unsigned nseg;      // segments in this level's queue
+    unsigned spl_ctr, bkt_ctr, tile_ctr, fin_ctr;
+    unsigned err;
+    unsigned pad[2];
+};
+enum : unsigned { kErrCapacity = 1, kErrTooLong = 2 };
+
+// ------------------------------------------------------------ classifiers
+// Equality-bucket classifier: bucket = 2*lb + (x == spl[lb]), lb = #{spl < x}.
+// Branch-free lower bound over a pow2-padded splitter table (padding is the
+// sentinel, which is never < x).
+template <typename K>
+__device__ __forceinline__ unsigned cls_eq(K x, const K* spl, unsigned m, unsigned span) {
+    unsigned pos = 0;
+    for (unsigned half = span >> 1; half >= 1; half >>= 1)
+        if (spl[pos + half - 1] < x) pos += half;
+    // pos is now #{spl[i] < x} restricted to span; equality check
+    const unsigned eq = (pos < m) && !(x < spl[pos]);
+    return 2 * pos + eq;
+}
+
+// (key, global index) classifier for the sharded sort: bucket = number of
+// splitters lexicographically below (x, gi); ties between equal keys are
+// broken by global index, which keeps few-unique inputs balanced.
+template <typename K>
+__device__ __forceinline__ unsigned cls_idx(K x, uint64_t gi, const K* spk, const uint64_t* spi, unsigned m) {
+    unsigned lo = 0, hi = m;
+    while (lo < hi) {
+        const unsigned mid = (lo + hi) >> 1;
+        const bool below = (spk[mid] < x) || (!(x < spk[mid]) && spi[mid] < gi);
+        if (below) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// --------------------------------------------------- smem bitonic (CTA-wide)
+// Plain ascending bitonic sort of P (pow2) keys (+payload) in shared memory.
+template <typename K, typename V, int NT>
+__device__ __forceinline__ void cta_bitonic(K* a, V* av, unsigned P) {
+    constexpr bool KV = HasVal<V>::value;
+    for (unsigned k = 2; k <= P; k <<= 1) {
+        for (unsigned j = k >> 1; j > 0; j >>= 1) {
+            for (unsigned i = threadIdx.x; i < P; i += NT) {
+                const unsigned ixj = i ^ j;
+                if (ixj > i) {
+                    const K x = a[i], y = a[ixj];
+                    const bool asc = (i & k) == 0;
+                    if (asc ? (y < x) : (x < y)) {
+                        a[i] = y;
+                        a[ixj] = x;
+                        if constexpr (KV) {
+                            V t = av[i];
+                            av[i] = av[ixj];
+                            av[ixj] = t;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------ init
+__global__ void qs_init_kernel(Seg* segs, Ctl* ctl, unsigned long long n) {
+    segs[0].start = 0;
+    segs[0].len = n;
+    ctl[0].nseg = 1;
+}
+
+// ------------------------------------------------------------ plan
+template <typename K, typename V>
+__global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ src, Seg* __restrict__ segs,
+                                                          Ctl* __restrict__ ctl, K* __restrict__ spl_pool,
+                                                          unsigned long long* __restrict__ bkt_pool,
+                                                          unsigned* __restrict__ tile_owner, unsigned cap_spl,
+                                                          unsigned cap_bkt, unsigned cap_tiles, uint64_t seed) {
+    constexpr int TILE = qs_tile<K>();
+    __shared__ K s_samp[kMaxSample];
+    __shared__ unsigned s_scan[kPlanNT / 32 + 1];
+    __shared__ unsigned s_off[3];
+    const unsigned nseg = ctl->nseg;
+    for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
+        const uint64_t start = segs[s].start, len = segs[s].len;
+        // aim global-level buckets at half the CTA-local capacity
+        const uint64_t mt64 = len / (FinCap<K, V>::value / 2);
+        const unsigned mt = (unsigned)max((uint64_t)2, min((uint64_t)kMaxSplit, mt64));
+        unsigned S = next_pow2_u32(16 * (mt + 1));
+        S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
+        for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
+            const uint64_t h = mix64(seed ^ mix64(start * 0x9E3779B97F4A7C15ULL + i));
+            s_samp[i] = src[start + (h % len)];
+        }
+        __syncthreads();
+        cta_bitonic<K, NoVal, kPlanNT>(s_samp, nullptr, S);
+        // candidate j = sample at quantile (j+1)/(mt+1); keep distinct values
+        K cand = K();
+        unsigned keep = 0;
+        if (threadIdx.x < mt) {
+            const unsigned q = (unsigned)(((uint64_t)(threadIdx.x + 1) * S) / (mt + 1));
+            cand = s_samp[q];
+            if (threadIdx.x == 0) keep = 1;
+            else {
+                const unsigned qp = (unsigned)(((uint64_t)threadIdx.x * S) / (mt + 1));
+                keep = (s_samp[qp] < cand) ? 1u : 0u;
+            }
+        }
+        unsigned m;
+        const unsigned rank = block_excl_scan<kPlanNT>(keep, s_scan, &m);
+        if (threadIdx.x == 0) {
+            const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
+            unsigned so = atomicAdd(&ctl->spl_ctr, m);
+            unsigned bo = atomicAdd(&ctl->bkt_ctr, 2 * m + 1);
+            unsigned to = atomicAdd(&ctl->tile_ctr, ntiles);
+            if (so + m > cap_spl || bo + 2 * m + 1 > cap_bkt || to + ntiles > cap_tiles) {
+                atomicOr(&ctl->err, kErrCapacity);
+                so = bo = to = 0;
+            }
+            s_off[0] = so;
+            s_off[1] = bo;
+            s_off[2] = to;
+            segs[s].spl_off = so;
+            segs[s].m = m;
+            segs[s].bkt_off = bo;
+            segs[s].tile_base = to;
+        }
+        __syncthreads();
+        if (keep) spl_pool[s_off[0] + rank] = cand;
+        for (unsigned b = threadIdx.x; b < 2 * m + 1; b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
+        const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
+        for (unsigned t = threadIdx.x; t < ntiles; t += kPlanNT) tile_owner[s_off[2] + t] = s;
+        __syncthreads();
+    }
+}
+
+// Load one segment's splitters into smem, padded with the sentinel to a pow2
+// span.  Returns the span.
+template <typename K, int NT>
+__device__ __forceinline__ unsigned load_splitters(K* s_spl, const K* spl_pool, unsigned off, unsigned m) {
+    const unsigned span = next_pow2_u32(m + 1);
+    for (unsigned i = threadIdx.x; i < span; i += NT) s_spl[i] = i < m ? spl_pool[off + i] : KeyTraits<K>::sentinel();
+    return span;
+}
+
+// ------------------------------------------------------------ hist
+template <typename K>
+__global__ void __launch_bounds__(kQsNT) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
+                                                        const Ctl* __restrict__ ctl, const unsigned* __restrict__ tile_owner,
+                                                        const K* __restrict__ spl_pool,
+                                                        unsigned long long* __restrict__ bkt_pool) {
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    __shared__ K s_spl[256];
+    __shared__ unsigned s_hist[kMaxBkt + 1];
+    const unsigned ntiles = ctl->tile_ctr;
+    unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
+    uint64_t sstart = 0, send = 0;
+    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const unsigned s = tile_owner[t];
+        __syncthreads();
+        if (s != cur) {
+            cur = s;
+            const Seg sg = segs[s];
+            m = sg.m;
+            bkt_off = sg.bkt_off;
+            tile_base = sg.tile_base;
+            sstart = sg.start;
+            send = sg.start + sg.len;
+            span = load_splitters<K, kQsNT>(s_spl, spl_pool, sg.spl_off, m);
+        }
+        const unsigned nb = 2 * m + 1;
+        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) s_hist[b] = 0;
+        __syncthreads();
+        const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
+        const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + threadIdx.x;
+            if (idx < tn) {
+                const K x = ld_stream(src + base + idx);
+                atomicAdd(&s_hist[cls_eq(x, s_spl, m, span)], 1u);
+            }
+        }
+        __syncthreads();
+        for (unsigned b = threadIdx.x; b < nb; b += kQsNT)
+            if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+    }
+}
+
+// ------------------------------------------------------------ emit
+// Exclusive scan of one u64 per thread over a CTA.
+template <int NT>
+__device__ __forceinline__ unsigned long long block_excl_scan_u64(unsigned long long v, unsigned long long* sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = NT / 32;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long t = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += t;
+    }
+    if (lane == 31) sm[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < NW ? sm[lane] : 0ull, wi = w;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xffffffffu, wi, d);
+            if (lane >= d) wi += t;
+        }
+        if (lane < NW) sm[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long r = sm[warp] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs, Ctl* __restrict__ ctl,
+                                                          Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
+                                                          unsigned long long* __restrict__ bkt_pool,
+                                                          Fin* __restrict__ fins, unsigned cap_seg, unsigned cap_fin,
+                                                          int dst_is_scratch) {
+    static_assert(kPlanNT >= kMaxBkt, "one thread per bucket");
+    constexpr uint32_t LOCAL = FinCap<K, V>::value;
+    __shared__ unsigned long long s_scan[kPlanNT / 32];
+    const unsigned nseg = ctl->nseg;
+    for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
+        const Seg sg = segs[s];
+        const unsigned nb = 2 * sg.m + 1;
+        const unsigned b = threadIdx.x;
+        const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + b] : 0ull;
+        const unsigned long long ex = block_excl_scan_u64<kPlanNT>(c, s_scan);
+        if (b < nb) {
+            const unsigned long long bstart = sg.start + ex;
+            bkt_pool[sg.bkt_off + b] = bstart;  // becomes the scatter cursor
+            if (c > 0) {
+                const bool final_ = (b & 1u) || c == 1;
+                if (final_) {
+                    if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
+                        const unsigned nch = (unsigned)((c + kCopyChunk - 1) / kCopyChunk);
+                        unsigned f = atomicAdd(&ctl->fin_ctr, nch);
+                        if (f + nch > cap_fin) {
+                            atomicOr(&ctl->err, kErrCapacity);
+                        } else {
+                            for (unsigned i = 0; i < nch; ++i) {
+                                const unsigned long long o = (unsigned long long)i * kCopyChunk;
+                                fins[f + i].start = bstart + o;
+                                fins[f + i].len = (unsigned)min((unsigned long long)kCopyChunk, c - o);
+                                fins[f + i].flags = 3u;
+                            }
+                        }
+                    }
+                } else if (c <= LOCAL) {
+                    unsigned f = atomicAdd(&ctl->fin_ctr, 1u);
+                    if (f >= cap_fin) {
+                        atomicOr(&ctl->err, kErrCapacity);
+                    } else {
+                        fins[f].start = bstart;
+                        fins[f].len = (unsigned)c;
+                        fins[f].flags = dst_is_scratch ? 1u : 0u;
+                    }
+                } else {
+                    unsigned q = atomicAdd(&ctl_next->nseg, 1u);
+                    if (q >= cap_seg) {
+                        atomicOr(&ctl->err, kErrCapacity);
+                    } else {
+                        next_segs[q].start = bstart;
+                        next_segs[q].len = c;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ scatter
+template <typename K, typename V>
+struct ScatterSmem {
+    static constexpr int TILE = qs_tile<K>();
+    K k[TILE];
+    typename std::conditional<HasVal<V>::value, V, char>::type v[HasVal<V>::value ? TILE : 1];
+    unsigned short b[TILE];
+    unsigned cnt[kMaxBkt + 1];
+    unsigned loc[kMaxBkt + 1];
+    unsigned long long gbase[kMaxBkt + 1];
+    K spl[256];
+    unsigned scan[kQsNT / 32 + 1];
+};
+
+// Rank IPT classified items of this thread inside the tile (smem atomics),
+// scan the bucket counts, reserve global runs and stage bucket-major.
+// Shared by the quicksort levels and the sharded bucket partition.
+template <typename K, typename V, int IPT>
+__device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)[IPT], const V (&v)[IPT],
+                                             const unsigned (&bk)[IPT], unsigned validmask, unsigned nb,
+                                             unsigned long long* cursor, K* dst_k, V* dst_v, unsigned tn) {
+    constexpr bool KV = HasVal<V>::value;
+    unsigned rank[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+        if ((validmask >> i) & 1u) rank[i] = atomicAdd(&sm.cnt[bk[i]], 1u);
+    __syncthreads();
+    // exclusive scan of counts over nb (<= 2*NT) buckets: 2 per thread
+    const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;
+    const unsigned c0 = b0 < nb ? sm.cnt[b0] : 0u, c1 = b1 < nb ? sm.cnt[b1] : 0u;
+    unsigned tot;
+    const unsigned ex = block_excl_scan<kQsNT>(c0 + c1, sm.scan, &tot);
+    if (b0 < nb) {
+        sm.loc[b0] = ex;
+        if (c0) sm.gbase[b0] = atomicAdd(&cursor[b0], (unsigned long long)c0);
+    }
+    if (b1 < nb) {
+        sm.loc[b1] = ex + c0;
+        if (c1) sm.gbase[b1] = atomicAdd(&cursor[b1], (unsigned long long)c1);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        if ((validmask >> i) & 1u) {
+            const unsigned slot = sm.loc[bk[i]] + rank[i];
+            sm.k[slot] = k[i];
+            if constexpr (KV) sm.v[slot] = v[i];
+            sm.b[slot] = (unsigned short)bk[i];
+        }
+    }
+    __syncthreads();
+    for (unsigned j = threadIdx.x; j < tn; j += kQsNT) {
+        const unsigned b = sm.b[j];
+        const unsigned long long pos = sm.gbase[b] + (j - sm.loc[b]);
+        dst_k[pos] = sm.k[j];
+        if constexpr (KV) dst_v[pos] = sm.v[j];
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+                                                           K* __restrict__ dst_k, V* __restrict__ dst_v,
+                                                           const Seg* __restrict__ segs, const Ctl* __restrict__ ctl,
+                                                           const unsigned* __restrict__ tile_owner,
+                                                           const K* __restrict__ spl_pool,
+                                                           unsigned long long* __restrict__ bkt_pool) {
+    constexpr bool KV = HasVal<V>::value;
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
+    const unsigned ntiles = ctl->tile_ctr;
+    unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
+    uint64_t sstart = 0, send = 0;
+    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const unsigned s = tile_owner[t];
+        __syncthreads();
+        if (s != cur) {
+            cur = s;
+            const Seg sg = segs[s];
+            m = sg.m;
+            bkt_off = sg.bkt_off;
+            tile_base = sg.tile_base;
+            sstart = sg.start;
+            send = sg.start + sg.len;
+            span = load_splitters<K, kQsNT>(sm.spl, spl_pool, sg.spl_off, m);
+        }
+        const unsigned nb = 2 * m + 1;
+        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
+        __syncthreads();
+        const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
+        const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
+        K k[IPT];
+        V v[IPT];
+        unsigned bk[IPT];
+        unsigned valid = 0;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + threadIdx.x;
+            if (idx < tn) {
+                k[i] = ld_stream(src_k + base + idx);
+                if constexpr (KV) v[i] = ld_stream(src_v + base + idx);
+                bk[i] = cls_eq(k[i], sm.spl, m, span);
+                valid |= 1u << i;
+            }
+        }
+        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, tn);
+    }
+}
+
+// ------------------------------------------------------------ finish
+template <typename K, typename V>
+struct FinSmem {
+    static constexpr uint32_t CAP = FinCap<K, V>::value;
+    K a[CAP];
+    K bb[CAP];
+    typename std::conditional<HasVal<V>::value, V, char>::type av[HasVal<V>::value ? CAP : 1];
+    typename std::conditional<HasVal<V>::value, V, char>::type bv[HasVal<V>::value ? CAP : 1];
+    K spl[256];
+    unsigned cnt[kMaxBkt + 1];
+    unsigned loc[kMaxBkt + 1];
+    unsigned scan[kFinNT / 32 + 1];
+};
+
+// CTA-local hybrid quicksort of one range (len <= CAP) from src into dst
+// (global), using shared memory as the working set.
+template <typename K, typename V>
+__device__ void fin_local_sort(FinSmem<K, V>& sm, const K* src_k, const V* src_v, K* dst_k, V* dst_v,
+                               uint64_t start, unsigned len, uint64_t seed, unsigned leaf) {
+    constexpr bool KV = HasVal<V>::value;
+    constexpr int NW = kFinNT / 32;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
+        sm.a[i] = src_k[start + i];
+        if constexpr (KV) sm.av[i] = src_v[start + i];
+    }
+    // sample into bb (free for now), sort it
+    unsigned S = next_pow2_u32(len / 8);
+    S = S < 256 ? 256 : (S > kFinSample ? kFinSample : S);
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < S; i += kFinNT) {
+        const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + i));
+        sm.bb[i] = sm.a[h % len];
+    }
+    __syncthreads();
+    cta_bitonic<K, NoVal, kFinNT>(sm.bb, nullptr, S);
+    unsigned mt = len / 96;
+    mt = mt < 2 ? 2 : (mt > 127 ? 127 : mt);
+    K cand = K();
+    unsigned keep = 0;
+    if (threadIdx.x < mt) {
+        const unsigned q = (unsigned)(((uint64_t)(threadIdx.x + 1) * S) / (mt + 1));
+        cand = sm.bb[q];
+        keep = threadIdx.x == 0 ? 1u
+                                : (sm.bb[(unsigned)(((uint64_t)threadIdx.x * S) / (mt + 1))] < cand ? 1u : 0u);
+    }
+    unsigned m;
+    const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
+    if (keep) sm.spl[rank] = cand;
+    const unsigned span = next_pow2_u32(m + 1);
+    const unsigned nb = 2 * m + 1;
+    __syncthreads();
+    for (unsigned i = m + threadIdx.x; i < span; i += kFinNT) sm.spl[i] = KeyTraits<K>::sentinel();
+    for (unsigned b = threadIdx.x; b < nb; b += kFinNT) sm.cnt[b] = 0;
+    __syncthreads();
+    // classify + rank (bucket id parked in bb as a temporary is not possible
+    // for K=int32 ranks, so recompute on the scatter pass)
+    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
+        const unsigned b = cls_eq(sm.a[i], sm.spl, m, span);
+        atomicAdd(&sm.cnt[b], 1u);
+    }
+    __syncthreads();
+    {
+        unsigned tot;
+        const unsigned c = threadIdx.x < nb ? sm.cnt[threadIdx.x] : 0u;
+        const unsigned ex = block_excl_scan<kFinNT>(c, sm.scan, &tot);
+        if (threadIdx.x < nb) {
+            sm.loc[threadIdx.x] = ex;
+            sm.cnt[threadIdx.x] = ex;  // becomes a running cursor
+        }
+    }
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
+        const K x = sm.a[i];
+        const unsigned b = cls_eq(x, sm.spl, m, span);
+        const unsigned slot = atomicAdd(&sm.cnt[b], 1u);
+        sm.bb[slot] = x;
+        if constexpr (KV) sm.bv[slot] = sm.av[i];
+    }
+    __syncthreads();
+    // every bucket: final -> copy; <= leaf -> warp bitonic; else below
+    for (unsigned b = warp; b < nb; b += NW) {
+        const unsigned lo = sm.loc[b], c = (b + 1 < nb ? sm.loc[b + 1] : len) - lo;
+        if (c == 0) continue;
+        if ((b & 1u) || c == 1) {
+            for (unsigned i = lane; i < c; i += 32) {
+                dst_k[start + lo + i] = sm.bb[lo + i];
+                if constexpr (KV) dst_v[start + lo + i] = sm.bv[lo + i];
+            }
+        } else if (c <= leaf) {
+            if constexpr (KV)
+                warp_sort_any2<K, V>(sm.bb + lo, sm.bv + lo, dst_k + start + lo, dst_v + start + lo, c);
+            else
+                warp_sort_any2<K, V>(sm.bb + lo, (const V*)nullptr, dst_k + start + lo, (V*)nullptr, c);
+        }
+    }
+    __syncthreads();
+    // rare: a range bucket above the leaf bound -> CTA bitonic in smem over a
+    // sentinel-padded copy in `a` (free by now; CAP is a power of two)
+    for (unsigned b = 0; b < nb; b += 2) {
+        const unsigned lo = sm.loc[b], c = (b + 1 < nb ? sm.loc[b + 1] : len) - lo;
+        if (c <= leaf) continue;
+        const unsigned P = next_pow2_u32(c);
+        for (unsigned i = threadIdx.x; i < P; i += kFinNT) {
+            sm.a[i] = i < c ? sm.bb[lo + i] : KeyTraits<K>::sentinel();
+            if constexpr (KV) sm.av[i] = i < c ? sm.bv[lo + i] : V();
+        }
+        __syncthreads();
+        if constexpr (KV) cta_bitonic<K, V, kFinNT>(sm.a, sm.av, P);
+        else cta_bitonic<K, NoVal, kFinNT>(sm.a, nullptr, P);
+        for (unsigned i = threadIdx.x; i < c; i += kFinNT) {
+            dst_k[start + lo + i] = sm.a[i];
+            if constexpr (KV) dst_v[start + lo + i] = sm.av[i];
+        }
+        __syncthreads();
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, const Ctl* __restrict__ ctl,
+                                                           K* __restrict__ data_k, V* __restrict__ data_v,
+                                                           const K* __restrict__ scr_k, const V* __restrict__ scr_v,
+                                                           uint64_t seed, unsigned leaf) {
+    constexpr bool KV = HasVal<V>::value;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FinSmem<K, V>& sm = *reinterpret_cast<FinSmem<K, V>*>(smem_raw);
+    const unsigned nf = ctl->fin_ctr;
+    for (unsigned d = blockIdx.x; d < nf; d += gridDim.x) {
+        const Fin f = fins[d];
+        const K* sk = (f.flags & 1u) ? scr_k : data_k;
+        const V* sv = (f.flags & 1u) ? scr_v : data_v;
+        if (f.flags & 2u) {
+            for (unsigned i = threadIdx.x; i < f.len; i += kFinNT) {
+                data_k[f.start + i] = sk[f.start + i];
+                if constexpr (KV) data_v[f.start + i] = sv[f.start + i];
+            }
+        } else if (f.len <= leaf) {
+            if (threadIdx.x < 32) warp_sort_any2<K, V>(sk + f.start, sv ? sv + f.start : nullptr, data_k + f.start,
+                                                       data_v ? data_v + f.start : nullptr, f.len);
+        } else {
+            fin_local_sort<K, V>(sm, sk, sv, data_k, data_v, f.start, f.len, seed, leaf);
+        }
+    }
+}
+
+// ------------------------------------------------------------ segments API
+// Batched bitonic over CSR segments (config 2): one warp per segment,
+// in place, lengths <= 256 (longer segments flag kErrTooLong, untouched).
+template <typename K, typename V>
+__global__ void __launch_bounds__(256) segsort_kernel(K* __restrict__ k, V* __restrict__ v,
+                                                      const long long* __restrict__ offs, uint64_t nseg,
+                                                      unsigned* __restrict__ err) {
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
+    for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps) {
+        const long long lo = offs[s], hi = offs[s + 1];
+        const long long len = hi - lo;
+        if (len < 2) continue;
+        if (len > 256) {
+            if ((threadIdx.x & 31) == 0) atomicOr(err, kErrTooLong);
+            continue;
+        }
+        warp_sort_any2<K, V>(k + lo, v ? v + lo : nullptr, k + lo, v ? v + lo : nullptr, (unsigned)len);
+    }
+}
+
+// ------------------------------------------------------------ bucket partition (sharded sort)
+// k-way partition of one array around m (key, global-index) splitters into
+// m+1 destination buckets.  Two kernels: histogram, then scatter; counts are
+// exclusive-scanned in between by bp_scan_kernel.
+template <typename K>
+__global__ void __launch_bounds__(kQsNT) bp_hist_kernel(const K* __restrict__ src, uint64_t n, uint64_t gofs,
+                                                        const K* __restrict__ spk, const uint64_t* __restrict__ spi,
+                                                        unsigned m, unsigned long long* __restrict__ counts) {
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    __shared__ K s_k[256];
+    __shared__ uint64_t s_i[256];
+    __shared__ unsigned s_hist[257];
+    for (unsigned i = threadIdx.x; i < m; i += kQsNT) {
+        s_k[i] = spk[i];
+        s_i[i] = spi[i];
+    }
+    const uint64_t ntiles = (n + TILE - 1) / TILE;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        __syncthreads();
+        for (unsigned b = threadIdx.x; b <= m; b += kQsNT) s_hist[b] = 0;
+        __syncthreads();
+        const uint64_t base = t * TILE;
+        const unsigned tn = (unsigned)min((uint64_t)TILE, n - base);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + threadIdx.x;
+            if (idx < tn) {
+                const K x = ld_stream(src + base + idx);
+                atomicAdd(&s_hist[cls_idx(x, gofs + base + idx, s_k, s_i, m)], 1u);
+            }
+        }
+        __syncthreads();
+        for (unsigned b = threadIdx.x; b <= m; b += kQsNT)
+            if (s_hist[b]) atomicAdd(&counts[b], (unsigned long long)s_hist[b]);
+    }
+}
+
+__global__ void bp_scan_kernel(const unsigned long long* __restrict__ counts, unsigned nb,
+                               unsigned long long* __restrict__ cursor) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        unsigned long long acc = 0;
+        for (unsigned b = 0; b < nb; ++b) {
+            cursor[b] = acc;
+            acc += counts[b];
+        }
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kQsNT) bp_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+                                                           K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t n,
+                                                           uint64_t gofs, const K* __restrict__ spk,
+                                                           const uint64_t* __restrict__ spi, unsigned m,
+                                                           unsigned long long* __restrict__ cursor) {
+    constexpr bool KV = HasVal<V>::value;
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
+    __shared__ uint64_t s_i[256];
+    for (unsigned i = threadIdx.x; i < m; i += kQsNT) {
+        sm.spl[i] = spk[i];
+        s_i[i] = spi[i];
+    }
+    const unsigned nb = m + 1;
+    const uint64_t ntiles = (n + TILE - 1) / TILE;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        __syncthreads();
+        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
+        __syncthreads();
+        const uint64_t base = t * TILE;
+        const unsigned tn = (unsigned)min((uint64_t)TILE, n - base);
+        K k[IPT];
+        V v[IPT];
+        unsigned bk[IPT];
+        unsigned valid = 0;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + threadIdx.x;
+            if (idx < tn) {
+                k[i] = ld_stream(src_k + base + idx);
+                if constexpr (KV) v[i] = ld_stream(src_v + base + idx);
+                bk[i] = cls_idx(k[i], gofs + base + idx, sm.spl, s_i, m);
+                valid |= 1u << i;
+            }
+        }
+        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, cursor, dst_k, dst_v, tn);
+    }
+}
+
+// Splitter selection for the sharded sort: sort the gathered (key, index)
+// samples lexicographically in smem and take nparts-1 evenly spaced ones.
+template <typename K>
+__global__ void __launch_bounds__(1024) select_splitters_kernel(const K* __restrict__ keys,
+                                                                const uint64_t* __restrict__ idx, unsigned count,
+                                                                unsigned nparts, K* __restrict__ out_k,
+                                                                uint64_t* __restrict__ out_i) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned P = next_pow2_u32(count);
+    K* sk = reinterpret_cast<K*>(smem_raw);
+    uint64_t* si = reinterpret_cast<uint64_t*>(smem_raw + sizeof(K) * P);
+    for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+        sk[i] = i < count ? keys[i] : KeyTraits<K>::sentinel();
+        si[i] = i < count ? idx[i] : ~0ull;
+    }
+    __syncthreads();
+    for (unsigned k = 2; k <= P; k <<= 1) {
+        for (unsigned j = k >> 1; j > 0; j >>= 1) {
+            for (unsigned i = threadIdx.x; i < P; i += blockDim.x) {
+                const unsigned ixj = i ^ j;
+                if (ixj > i) {
+                    const K x = sk[i], y = sk[ixj];
+                    const uint64_t xi = si[i], yi = si[ixj];
+                    const bool y_lt_x = (y < x) || (!(x < y) && yi < xi);
+                    const bool asc = (i & k) == 0;
+                    if (asc ? y_lt_x : !y_lt_x) {
+                        sk[i] = y; sk[ixj] = x;
+                        si[i] = yi; si[ixj] = xi;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (unsigned r = threadIdx.x + 1; r < nparts; r += blockDim.x) {
+        const unsigned q = (unsigned)(((uint64_t)r * count) / nparts);
+        out_k[r - 1] = sk[q];
+        out_i[r - 1] = si[q];
+    }
+}
+
+}  // namespace vx

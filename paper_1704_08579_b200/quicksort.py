@@ -1,0 +1,103 @@
+"""Hybrid quicksort API (mirror of vexsort/quicksort.py).
+
+``sort`` / ``sort_with_config`` keep the reference's names, config object,
+validation and in-place semantics (quicksort.py:28-52, 115-143).  The work
+runs in the device-side hybrid quicksort of csrc/qsort.cuh: sampled
+multi-pivot partition levels over a device work queue, then a CTA-local
+partition plus the bitonic network on every range <= sort_bound.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+from ._lib import SortConfigC, check, lib
+from ._region import check_region, dev_ptr, host_ptr, stream_of, workspace
+from .lanes import get_backend, is_device
+
+__all__ = ["SortConfig", "sort", "sort_with_config", "select_pivot", "MAX_PACKS"]
+
+MAX_PACKS = 16  # smallsort.py:40
+_PIVOT_STRATEGIES = ("median3", "middle", "random")
+_U64 = (1 << 64) - 1
+
+
+@dataclass(frozen=True)
+class SortConfig:
+    """Tuning knobs (quicksort.py:28-46).
+
+    sort_bound: largest range handed to the bitonic network (default
+    16*lanes: 256 int32 / 128 float64; must not exceed it).  pivot_strategy
+    is validated like the reference's; the B200 driver always samples its
+    pivots (seeded by pivot_seed), so the strategy cannot change the (unique)
+    sorted output.  skip_empty_stores / swap_buffered are CPU store-pattern
+    options of the reference partition and are accepted as no-ops.
+    """
+
+    sort_bound: int | None = None
+    pivot_strategy: str = "median3"
+    skip_empty_stores: bool = False
+    swap_buffered: bool = False
+    backend: str = "auto"
+    pivot_seed: int = 0
+
+    def __post_init__(self):
+        if self.pivot_strategy not in _PIVOT_STRATEGIES:
+            raise ValueError(f"unknown pivot strategy {self.pivot_strategy!r}")
+
+
+def _resolve_bound(config: SortConfig, lanes: int) -> int:
+    bound = config.sort_bound if config.sort_bound is not None else MAX_PACKS * lanes
+    assert 1 <= bound <= MAX_PACKS * lanes, "sort_bound exceeds small-sort capacity"
+    return bound
+
+
+def select_pivot(region, lo: int, hi: int, strategy: str = "median3", lcg_state: int | None = None) -> int:
+    """Index of the pivot for the inclusive range [lo, hi] (quicksort.py:55-74).
+    Host-side helper (reads at most three elements), used e.g. to pick the
+    config-3 pivot."""
+    assert lo <= hi
+    if strategy == "middle":
+        return (lo + hi) // 2
+    if strategy == "random":
+        state = (lcg_state if lcg_state is not None else 0) & _U64
+        return lo + state % (hi - lo + 1)
+    mid = (lo + hi) // 2
+    a, b, c = (region[i].item() if hasattr(region[i], "item") else region[i] for i in (lo, mid, hi))
+    if b <= a <= c or c <= a <= b:
+        return lo
+    if a <= b <= c or c <= b <= a:
+        return mid
+    return hi
+
+
+def _cfg(config: SortConfig, bound: int) -> SortConfigC:
+    return SortConfigC(bound, _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),
+                       int(config.swap_buffered), 0, int(config.pivot_seed) & _U64)
+
+
+def sort_with_config(region, config: SortConfig) -> None:
+    """Sort a region ascending in place under an explicit configuration."""
+    n = len(region)
+    if n < 2:
+        return
+    kind = check_region(region)
+    backend = get_backend(config.backend, kind)
+    bound = _resolve_bound(config, backend.lanes)
+    L = lib()
+    if is_device(region):
+        ws = workspace(L.vx_sort_workspace_bytes(kind.code, 0, n), region.device)
+        cfg = _cfg(config, bound)
+        check(L.vx_sort(kind.code, dev_ptr(region), None, n, ctypes.byref(cfg), dev_ptr(ws), ws.numel(),
+                        stream_of(region)), "sort")
+        return
+    check(L.vx_host_quicksort(kind.code, host_ptr(region), n, backend.lanes, bound,
+                              _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),
+                              int(config.swap_buffered), int(config.pivot_seed) & _U64), "sort")
+
+
+def sort(region, config: SortConfig | None = None) -> None:
+    """Sort a region of int32 or float64 ascending, in place (quicksort.py:137-143).
+    NaN elements are unsupported."""
+    sort_with_config(region, config or SortConfig())

@@ -1,0 +1,528 @@
+"""GPU parity: the B200 kernels (through the C ABI) against the CPU oracle
+and the reference-generated golden fixtures.
+
+Rules: int32 / float64 sorts bit-exact; partitions: exact
+boundary, side predicates, multiset (the reference's layout is a CPU
+artefact); kv: keys bit-exact, keys_in[vals_out] == keys_out and vals_out a
+permutation (pair-multiset equality).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1704_08579_b200 as vx  # noqa: E402
+
+DEV = "cuda"
+
+
+def _d(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _h(t):
+    return t.cpu().numpy()
+
+
+def _load(golden_dir, name):
+    return np.load(os.path.join(golden_dir, name))
+
+
+def _ids(z):
+    return sorted({k.rsplit("_", 1)[0] for k in z.files})
+
+
+def _digests(golden_dir):
+    with open(os.path.join(golden_dir, "config_digests.json")) as f:
+        return json.load(f)
+
+
+def _digest(*arrs):
+    from make_golden import digest
+
+    return digest(*arrs)
+
+
+# ------------------------------------------------------------------ sort
+
+
+def test_reference_example():
+    for dt in (np.int32, np.float64):
+        t = _d(np.array([3, 1, 2, 0, 5], dtype=dt))
+        vx.sort(t)
+        assert _h(t).tolist() == [0, 1, 2, 3, 5]
+
+
+def test_trivial_regions():
+    for dt in (np.int32, np.float64):
+        for data in ([], [4], [7, 7, 7, 7]):
+            t = _d(np.array(data, dtype=dt))
+            vx.sort(t)
+            assert _h(t).tolist() == sorted(data)
+
+
+def test_golden_sort_cases_device(golden_dir):
+    z = _load(golden_dir, "sort_cases.npz")
+    for cid in _ids(z):
+        x, want = z[cid + "_in"], z[cid + "_out"]
+        for strategy in ("median3", "middle", "random"):
+            t = _d(x)
+            vx.sort(t, vx.SortConfig(pivot_strategy=strategy, pivot_seed=9))
+            assert np.array_equal(_h(t), want), (cid, strategy)
+
+
+def test_golden_sort_cases_host_buffers(golden_dir):
+    # numpy arrays in, in place, through the host-buffer C ABI (vx_host_*)
+    z = _load(golden_dir, "sort_cases.npz")
+    for cid in _ids(z):
+        x, want = z[cid + "_in"], z[cid + "_out"]
+        a = x.copy()
+        vx.sort(a)
+        assert np.array_equal(a, want), cid
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_random_sizes_match_oracle(dt):
+    rng = np.random.default_rng(1)
+    sizes = rng.integers(0, 70000, size=30).tolist() + [0, 1, 2, 255, 256, 257, 4095, 4096, 4097, 8191, 8192,
+                                                       8193, 16385, 100003]
+    for n in sizes:
+        x = (rng.integers(-(2**31), 2**31 - 1, size=n, dtype=np.int64, endpoint=True).astype(np.int32)
+             if dt == np.int32 else rng.uniform(-1e9, 1e9, size=n))
+        t = _d(x)
+        vx.sort(t)
+        want = x.copy()
+        oracle.sort(want)
+        assert np.array_equal(_h(t), want), n
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+@pytest.mark.parametrize("n", [1 << 16, 1 << 20])
+def test_adversarial_patterns(dt, n):
+    pats = {
+        "sorted": np.arange(n),
+        "reverse": np.arange(n)[::-1].copy(),
+        "sawtooth": np.tile(np.arange(37), n // 37 + 1)[:n],
+        "few-distinct": np.random.default_rng(5).integers(0, 8, size=n),
+        "all-equal": np.full(n, 7),
+        "two-values": np.random.default_rng(6).integers(0, 2, size=n) * 1000,
+        "organ-pipe": np.concatenate([np.arange(n // 2), np.arange(n - n // 2)[::-1]]),
+    }
+    for name, base in pats.items():
+        x = base.astype(dt)
+        t = _d(x)
+        vx.sort(t)
+        assert np.array_equal(_h(t), np.sort(x)), name
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_extreme_values_and_sentinels(dt):
+    rng = np.random.default_rng(77)
+    for n in (100, 300, 5000, 50000, 300000):
+        x = rng.integers(-50, 50, size=n).astype(dt)
+        if dt == np.int32:
+            x[::7] = np.iinfo(np.int32).max
+            x[3::11] = np.iinfo(np.int32).min
+        else:
+            x[::7] = np.inf
+            x[3::11] = -np.inf
+            x[5::13] = np.finfo(np.float64).max
+        t = _d(x)
+        vx.sort(t)
+        assert np.array_equal(_h(t), np.sort(x)), n
+
+
+def test_custom_sort_bound_and_flags():
+    rng = np.random.default_rng(3)
+    for dt, lanes in ((np.int32, 16), (np.float64, 8)):
+        x = rng.integers(-100, 100, size=40000).astype(dt)
+        for cfg in (vx.SortConfig(sort_bound=lanes), vx.SortConfig(sort_bound=1),
+                    vx.SortConfig(skip_empty_stores=True, swap_buffered=True)):
+            t = _d(x)
+            vx.sort(t, cfg)
+            assert np.array_equal(_h(t), np.sort(x))
+
+
+def test_sort_bound_validation():
+    with pytest.raises(AssertionError):
+        vx.sort(_d(np.zeros(300, dtype=np.float64)), vx.SortConfig(sort_bound=129))
+    with pytest.raises(ValueError):
+        vx.SortConfig(pivot_strategy="bogus")
+
+
+def test_sort_is_idempotent():
+    x = np.random.default_rng(21).integers(-(2**31), 2**31 - 1, size=200000, dtype=np.int32)
+    t = _d(x)
+    vx.sort(t)
+    once = _h(t).copy()
+    vx.sort(t)
+    assert np.array_equal(_h(t), once)
+
+
+def test_sort_views_in_place():
+    x = np.random.default_rng(2).integers(-1000, 1000, size=50000).astype(np.int32)
+    t = _d(x)
+    vx.sort(t[1000:40001])
+    want = x.copy()
+    want[1000:40001] = np.sort(want[1000:40001])
+    assert np.array_equal(_h(t), want)
+
+
+def test_c1_digest_matches_reference(golden_dir):
+    d = _digests(golden_dir)["c1_i32_2^20"]
+    x = inputs.c1_input()
+    assert _digest(x) == d["in"]
+    t = _d(x)
+    vx.sort(t)
+    assert _digest(_h(t)) == d["out"]
+
+
+@pytest.mark.parametrize("dist", ["uniform", "sorted", "reverse", "few"])
+def test_c5_reduced_digests_match_reference(golden_dir, dist):
+    dig = _digests(golden_dir)
+    for tag, dt in (("i32", np.int32), ("f64", np.float64)):
+        x = inputs.c5_input(dt, dist, n=1 << 16)
+        d = dig[f"c5_{tag}_{dist}_2^16"]
+        assert _digest(x) == d["in"]
+        t = _d(x)
+        vx.sort(t)
+        assert _digest(_h(t)) == d["out"]
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_large_sort_2_24(dt):
+    n = 1 << 24
+    rng = np.random.default_rng(11)
+    x = (rng.integers(-(2**31), 2**31 - 1, size=n, dtype=np.int32, endpoint=True) if dt == np.int32
+         else rng.uniform(-1e6, 1e6, size=n))
+    t = _d(x)
+    vx.sort(t)
+    assert np.array_equal(_h(t), np.sort(x))
+
+
+def test_full_size_c5_distributions_properties():
+    # size-independent properties at 2^26 (sortedness + checksum of the
+    # multiset) for the four C5 distributions generated on the device
+    import ctypes
+
+    L = vx._lib.lib()
+    n = 1 << 26
+    for dist in (0, 1, 2, 3):
+        t = torch.empty(n, dtype=torch.int32, device=DEV)
+        L.vx_generate(0, dist, ctypes.c_void_p(t.data_ptr()), n, 1, 0, n,
+                      ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        ref = torch.sort(t.to(torch.int64))[0]  # independent comparator (library sort, test only)
+        vx.sort(t)
+        assert torch.equal(t.to(torch.int64), ref), dist
+
+
+# ------------------------------------------------------------- partition
+
+
+def test_partition_example():
+    for dt in (np.int32, np.float64):
+        t = _d(np.array([3, 1, 2, 0, 5], dtype=dt))
+        b = vx.partition_region(t, 2)
+        assert b == 3
+        a = _h(t)
+        assert sorted(a[:3].tolist()) == [0, 1, 2] and sorted(a[3:].tolist()) == [3, 5]
+
+
+def _check_partitioned(arr, before, pivot, b):
+    assert 0 <= b <= len(arr)
+    assert np.all(arr[:b] <= pivot)
+    assert np.all(arr[b:] > pivot)
+    assert np.array_equal(np.sort(arr), np.sort(before))
+    assert b == int(np.count_nonzero(before <= pivot))
+
+
+def test_golden_partition_cases(golden_dir):
+    z = _load(golden_dir, "partition_cases.npz")
+    for cid in _ids(z):
+        x = z[cid + "_in"]
+        b_want, opt_a, opt_b = (int(v) for v in z[cid + "_meta"])
+        pivot = float(z[cid + "_pivot"][0])
+        if x.dtype == np.int32:
+            pivot = int(pivot)
+        want = z[cid + "_out"]
+        t = _d(x)
+        b = vx.partition_region(t, pivot, skip_empty_stores=bool(opt_a), swap_buffered=bool(opt_b))
+        assert b == b_want, cid
+        got = _h(t)
+        _check_partitioned(got, x, pivot, b)
+        # same sides as the reference's own layout (as multisets)
+        assert np.array_equal(np.sort(got[:b]), np.sort(want[:b]))
+        assert np.array_equal(np.sort(got[b:]), np.sort(want[b:]))
+        # host-buffer path too
+        a = x.copy()
+        assert vx.partition_region(a, pivot) == b_want
+        _check_partitioned(a, x, pivot, b_want)
+
+
+def test_partition_empty_tiny_all_low_all_high():
+    for dt in (np.int32, np.float64):
+        for n in (0, 1, 2, 5, 33, 4097):
+            x = np.full(n, 3, dtype=dt)
+            assert vx.partition_region(_d(x), 2) == 0
+            assert vx.partition_region(_d(x), 3) == n  # ties go low
+        rng = np.random.default_rng(0)
+        x = rng.integers(-10, 10, size=100000).astype(dt)
+        assert vx.partition_region(_d(x), 10) == 100000
+        assert vx.partition_region(_d(x), -11) == 0
+
+
+def test_partition_pivot_semantics_int32():
+    x = np.arange(-10, 10, dtype=np.int32)
+    assert vx.partition_region(_d(x), 2.5) == 13      # floor(2.5) = 2
+    assert vx.partition_region(_d(x), -2.5) == 7      # floor(-2.5) = -3
+    assert vx.partition_region(_d(x), 2**40) == 20
+    assert vx.partition_region(_d(x), -(2**40)) == 0
+    assert vx.partition_region(_d(x), float("nan")) == 0
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_partition_random_sweep_vs_oracle(dt):
+    rng = np.random.default_rng(42)
+    for _ in range(60):
+        n = int(rng.integers(0, 300000))
+        x = rng.integers(-100, 100, size=n).astype(dt)
+        pivot = int(rng.integers(-110, 110))
+        t = _d(x)
+        b = vx.partition_region(t, pivot)
+        assert b == oracle.partition_region(x.copy(), pivot)
+        _check_partitioned(_h(t), x, pivot, b)
+
+
+def test_partition_misaligned_views_and_out():
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(100003)
+    t = _d(x)
+    v = t[3:]  # not 16-byte aligned -> scalar-load kernel variant
+    out = torch.empty_like(v)
+    b = vx.partition_region(v, 0.1, out=out)
+    _check_partitioned(_h(out), x[3:], 0.1, b)
+    assert np.array_equal(_h(t), x)  # out= leaves the input untouched
+
+
+def test_c3_reduced_digest_matches_reference(golden_dir):
+    d = _digests(golden_dir)["c3_f64_2^20"]
+    x = inputs.c3_input(n=1 << 20)
+    assert _digest(x) == d["in"]
+    pivot = float(x[oracle.median3_index(x, 0, len(x) - 1)])
+    assert pivot == d["pivot"]
+    t = _d(x)
+    b = vx.partition_region(t, pivot)
+    assert b == d["split"]
+    got = _h(t)
+    assert _digest(np.sort(got[:b])) == d["sorted_low"]
+    assert _digest(np.sort(got[b:])) == d["sorted_high"]
+
+
+def test_c3_full_size_split_exact():
+    # 2^28 f64 N(0,1) generated on device; split vs an independent count
+    import ctypes
+
+    n = 1 << 28
+    L = vx._lib.lib()
+    x = torch.empty(n, dtype=torch.float64, device=DEV)
+    L.vx_generate(1, 4, ctypes.c_void_p(x.data_ptr()), n, 3, 0, n,
+                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    pivot = float(x[vx.select_pivot(x, 0, n - 1)].item())
+    out = torch.empty_like(x)
+    b = vx.partition_region(x, pivot, out=out)
+    assert b == int((x <= pivot).sum().item())
+    assert bool((out[:b] <= pivot).all()) and bool((out[b:] > pivot).all())
+    assert float(out.sum().item()) == pytest.approx(float(x.sum().item()), rel=1e-9, abs=1e-6)
+    assert torch.equal(torch.sort(out[:b])[0], torch.sort(x[x <= pivot])[0])
+
+
+# -------------------------------------------------------------- small sort
+
+
+def test_golden_smallsort_all_lengths(golden_dir):
+    z = _load(golden_dir, "smallsort_cases.npz")
+    for cid in _ids(z):
+        x, want = z[cid + "_in"], z[cid + "_out"]
+        t = _d(x)
+        vx.sort_small_region(t)
+        assert np.array_equal(_h(t), want), cid
+
+
+def test_smallsort_rejects_oversize():
+    with pytest.raises(AssertionError):
+        vx.sort_small_region(_d(np.zeros(257, dtype=np.int32)))
+    with pytest.raises(AssertionError):
+        vx.sort_small_region(_d(np.zeros(129, dtype=np.float64)))
+
+
+def test_padding_value_never_leaks():
+    for dt, sent in ((np.int32, 2**31 - 1), (np.float64, np.inf)):
+        for n in (1, 7, 19, 128):
+            t = _d(np.full(n, sent, dtype=dt))
+            vx.sort_small_region(t)
+            assert np.all(_h(t) == sent)
+
+
+@pytest.mark.parametrize("tag,dt", [("i32", np.int32), ("f64", np.float64)])
+def test_c2_reduced_digest_matches_reference(golden_dir, tag, dt):
+    d = _digests(golden_dir)[f"c2_{tag}_2^12seg"]
+    offs, vals = inputs.c2_input(dt, nseg=1 << 12)
+    assert _digest(offs, vals) == d["in"]
+    t = _d(vals)
+    vx.sort_segments(t, _d(offs))
+    assert _digest(_h(t)) == d["out"]
+
+
+def test_segments_every_length_and_payload():
+    rng = np.random.default_rng(9)
+    lens = np.concatenate([np.arange(0, 257), rng.integers(0, 257, size=3000)])
+    offs = np.zeros(len(lens) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    for dt, vdt in ((np.int32, np.int32), (np.float64, np.int64)):
+        k = rng.integers(-20, 20, size=int(offs[-1])).astype(dt)
+        v = np.arange(len(k), dtype=vdt)
+        tk, tv = _d(k), _d(v)
+        vx.sort_segments(tk, _d(offs), tv)
+        gk, gv = _h(tk), _h(tv)
+        for s in range(len(lens)):
+            lo, hi = offs[s], offs[s + 1]
+            assert np.array_equal(gk[lo:hi], np.sort(k[lo:hi]))
+            assert np.array_equal(np.sort(gv[lo:hi]), v[lo:hi])
+        assert np.array_equal(k[gv], gk)
+
+
+def test_segments_reject_long():
+    offs = np.array([0, 10, 300], dtype=np.int64)
+    with pytest.raises(AssertionError):
+        vx.sort_segments(_d(np.zeros(300, dtype=np.int32)), _d(offs))
+
+
+# ---------------------------------------------------------------------- kv
+
+
+def _check_kv(k_in, k_out, v_out):
+    assert np.array_equal(k_out, np.sort(k_in))
+    assert np.array_equal(k_in[v_out], k_out)
+    assert np.array_equal(np.sort(v_out), np.arange(len(k_in)))
+
+
+def test_golden_kv_cases(golden_dir):
+    z = _load(golden_dir, "kv_cases.npz")
+    for tag, vdt in (("i32", np.int32), ("f64", np.int64)):
+        for i in range(80):
+            key = f"sort_{tag}_{i}"
+            if key + "_kin" not in z.files:
+                continue
+            kin = z[key + "_kin"]
+            tk, tv = _d(kin), _d(np.arange(len(kin), dtype=vdt))
+            vx.kv_sort(tk, tv)
+            assert np.array_equal(_h(tk), z[key + "_kout"])
+            _check_kv(kin, _h(tk), _h(tv))
+            # kv partition: boundary exact, sides as multisets of pairs
+            pk = f"part_{tag}_{i}"
+            b_want, pivot = (int(t) for t in z[pk + "_meta"])
+            tk, tv = _d(kin), _d(np.arange(len(kin), dtype=vdt))
+            b = vx.kv_partition_region(tk, tv, pivot)
+            assert b == b_want
+            gk, gv = _h(tk), _h(tv)
+            assert np.array_equal(kin[gv], gk)
+            assert np.all(gk[:b] <= pivot) and np.all(gk[b:] > pivot)
+            assert np.array_equal(np.sort(gv[:b]), np.sort(z[pk + "_vout"][:b]))
+
+
+def test_kv_host_buffers_and_alias():
+    rng = np.random.default_rng(5)
+    k = rng.integers(0, 50, size=20000).astype(np.int32)
+    v = np.arange(len(k), dtype=np.int32)
+    k2, v2 = k.copy(), v.copy()
+    vx.sort_kv(k2, v2)
+    _check_kv(k, k2, v2)
+
+
+def test_kv_width_rule():
+    with pytest.raises(AssertionError):
+        vx.kv_sort(_d(np.zeros(10, dtype=np.int32)), _d(np.zeros(10, dtype=np.int64)))
+    with pytest.raises(AssertionError):
+        vx.kv_sort(_d(np.zeros(10, dtype=np.int32)), _d(np.zeros(11, dtype=np.int32)))
+
+
+def test_c4_reduced_digest_and_pairs(golden_dir):
+    d = _digests(golden_dir)["c4_kv_2^18"]
+    k0, v0 = inputs.c4_input(n=1 << 18)
+    assert _digest(k0, v0) == d["in"]
+    tk, tv = _d(k0), _d(v0)
+    vx.kv_sort(tk, tv)
+    assert _digest(_h(tk)) == d["keys"]
+    _check_kv(k0, _h(tk), _h(tv))
+
+
+def test_kv_f64_large():
+    rng = np.random.default_rng(8)
+    n = 1 << 22
+    k = rng.integers(-1000, 1000, size=n).astype(np.float64)
+    tk, tv = _d(k), _d(np.arange(n, dtype=np.int64))
+    vx.kv_sort(tk, tv)
+    _check_kv(k, _h(tk), _h(tv))
+
+
+def test_c4_full_size_properties():
+    # 2^28 pairs: keys sorted (vs library sort as an independent comparator),
+    # values a permutation with keys_in[vals_out] == keys_out
+    import ctypes
+
+    n = 1 << 28
+    L = vx._lib.lib()
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    k = torch.empty(n, dtype=torch.int32, device=DEV)
+    v = torch.empty(n, dtype=torch.int32, device=DEV)
+    L.vx_generate(0, 5, ctypes.c_void_p(k.data_ptr()), n, 4, 0, n, st)
+    L.vx_generate(0, 6, ctypes.c_void_p(v.data_ptr()), n, 4, 0, n, st)
+    k0 = k.clone()
+    vx.kv_sort(k, v)
+    assert torch.equal(k, torch.sort(k0)[0])
+    assert torch.equal(k0[v.long()], k)
+    assert bool((torch.bincount(v.long(), minlength=n) == 1).all())
+
+
+# ---------------------------------------------------------- sharded (P=1)
+
+
+def test_sharded_single_rank_and_bucket_partition():
+    import torch.distributed as dist
+
+    assert not dist.is_initialized()
+    rng = np.random.default_rng(12)
+    x = rng.integers(0, 16, size=300000).astype(np.int32)
+    out = vx.sharded_sort(_d(x))
+    assert np.array_equal(_h(out), np.sort(x))
+    # bucket partition with (key, index) splitters against a numpy model
+    from paper_1704_08579_b200.sharded import B200Ops
+
+    ops = B200Ops()
+    gofs = 12345
+    pos = np.sort(rng.choice(len(x), size=4000, replace=False))
+    sk, si = ops.select_splitters(_d(x[pos]), _d(pos + gofs), 8)
+    order = np.lexsort((pos + gofs, x[pos]))
+    q = [(r * 4000) // 8 for r in range(1, 8)]
+    assert np.array_equal(_h(sk), x[pos][order][q]) and np.array_equal(_h(si), (pos + gofs)[order][q])
+    parted, counts = ops.bucket_partition(_d(x), gofs, sk, si)
+    gk, gi = _h(sk), _h(si)
+    gidx = np.arange(len(x)) + gofs
+    dest = np.zeros(len(x), dtype=np.int64)
+    for j in range(len(gk)):
+        dest += (gk[j] < x) | ((gk[j] == x) & (gi[j] < gidx))
+    want_counts = np.bincount(dest, minlength=8)
+    assert np.array_equal(_h(counts), want_counts)
+    p = _h(parted)
+    o = 0
+    for b in range(8):
+        assert np.array_equal(np.sort(p[o:o + want_counts[b]]), np.sort(x[dest == b]))
+        o += want_counts[b]
