@@ -282,7 +282,7 @@ def test_partition_empty_tiny_all_low_all_high():
 def test_partition_pivot_semantics_int32():
     x = np.arange(-10, 10, dtype=np.int32)
     assert vx.partition_region(_d(x), 2.5) == 13      # floor(2.5) = 2
-    assert vx.partition_region(_d(x), -2.5) == 7      # floor(-2.5) = -3
+    assert vx.partition_region(_d(x), -2.5) == 8      # floor(-2.5) = -3: -10..-3
     assert vx.partition_region(_d(x), 2**40) == 20
     assert vx.partition_region(_d(x), -(2**40)) == 0
     assert vx.partition_region(_d(x), float("nan")) == 0
