@@ -1,0 +1,549 @@
+"""Benchmark of the B200 hybrid sort (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c5_i32_uniform|...] [--n N_GLOBAL]
+
+Default workload (the BASELINE.json metric "Gelements/s sorted (int32/f64/kv)
+at 1-8 B200"): config 5, the sharded sort of n = 2^32 int32 i.i.d. uniform
+over the full range, global n fixed across 1/2/4/8 ranks ("strong"); one
+step = one complete sort of the global array (at N=1 the local hybrid
+quicksort, at N>1 sample sort: splitters + bucket partition + NCCL
+all-to-all + local sort).  Inputs are generated on the device from a seeded
+counter hash and stay resident; every step sorts the same pristine input
+out of place (16 GiB >> the 126 MB L2, so no L2 flush is needed).
+
+Other workloads (--workload): sort_i32_2^28, sort_f64_2^28, c1 (int32 2^20),
+c2_i32 / c2_f64 (2^20 CSR segments of U{1..256}), c3 (f64 2^28 N(0,1)
+partition around median-of-3), c4 (kv 2^28), c5_{i32,f64}_{uniform,sorted,
+reverse,few}.
+
+value  = elements / max-over-ranks device time of the K timed steps.
+e2e    = the same metric through the public API with HOST buffers: pinned
+         host input -> device -> sort -> host, copies inside the timed region
+         (N=1 sorts: the reference-facing C-ABI host entry vx_host_quicksort).
+roofline = the dominant kernel class: algorithmic bytes (one read + one
+         write of every element it processed) / its summed
+         CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline = the CPU oracle (C port of the reference's _kernels.py,
+         OpenMP task-parallel variant, identical output) on a bounded sample.
+--impl reference: only that CPU port, rank 0, same metric and unit.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+
+METRIC = "Gelements/s sorted (int32/f64/kv) at 1-8 B200; % of HBM/NVLink roofline"
+PEAK_FALLBACK = 6650.0
+NVL_GBS = 900.0  # per direction, spec (no measured all-to-all peak yet)
+
+# generator dist codes of vx_generate
+DIST = {"uniform": 0, "sorted": 1, "reverse": 2, "few": 3, "normal": 4, "u31": 5, "index": 6}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return PEAK_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def workload_spec(name: str, n_override: int | None):
+    """-> dict(kind, dtype, n, ...)."""
+    if name.startswith("c5_"):
+        _, t, dist = name.split("_")
+        n = n_override or (1 << 32 if t == "i32" else 1 << 31)
+        return dict(kind="sharded", dtype=t, dist=dist, n=n, scaling="strong")
+    if name.startswith("sort_"):
+        t = name.split("_")[1]
+        n = n_override or (1 << 28)
+        return dict(kind="sort", dtype=t, dist="uniform", n=n, scaling="weak")
+    if name == "c1":
+        return dict(kind="sort", dtype="i32", dist="uniform", n=n_override or (1 << 20), scaling="weak")
+    if name in ("c2_i32", "c2_f64"):
+        return dict(kind="segments", dtype=name[3:], nseg=n_override or (1 << 20), scaling="weak")
+    if name == "c3":
+        return dict(kind="partition", dtype="f64", dist="normal", n=n_override or (1 << 28), scaling="weak")
+    if name == "c4":
+        return dict(kind="kv", dtype="i32", dist="u31", n=n_override or (1 << 28), scaling="weak")
+    raise SystemExit(f"unknown workload {name}")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50", "-i",
+                 str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        loaded = [r for r in rows if r[0] > 0.5 * r[1]] or rows
+        return {"sm_mhz": statistics.median(r[0] for r in loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(loaded)}
+
+
+# --------------------------------------------------------------- utilities
+def dist_setup(n_gpus):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus and world > 1:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.barrier()
+
+
+def allmax(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gen(L, dtype_code, dist_code, t, seed, gofs, gn):
+    import torch
+
+    L.vx_generate(dtype_code, dist_code, ctypes.c_void_p(t.data_ptr()), t.numel(), seed, gofs, gn,
+                  ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+
+
+def prof_read(L):
+    n = 8
+    la = (ctypes.c_int64 * n)()
+    ms = (ctypes.c_double * n)()
+    el = (ctypes.c_uint64 * n)()
+    L.vx_profile_read(la, ms, el, n)
+    return list(la), list(ms), list(el)
+
+
+CLASSES = ["qs_plan", "qs_hist", "qs_emit", "qs_scatter", "qs_finish", "partition2", "segsort", "bucket_partition"]
+KERNEL_REGEX = {"qs_plan": "qs_plan_kernel", "qs_hist": "qs_hist_kernel", "qs_emit": "qs_emit_kernel",
+                "qs_scatter": "qs_scatter_kernel", "qs_finish": "qs_finish_kernel",
+                "partition2": "partition2_kernel", "segsort": "segsort_kernel",
+                "bucket_partition": "bp_scatter_kernel"}
+
+
+def ncu_traffic(kernel_class):
+    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(KERNEL_REGEX.get(kernel_class, kernel_class))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------- our workloads
+def run_ours(args, spec, rank, world, local):
+    import numpy as np
+    import torch
+
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200 import _lib
+
+    L = _lib.lib()
+    dev = torch.device("cuda", local)
+    tdt = torch.int32 if spec["dtype"] == "i32" else torch.float64
+    dcode = 0 if spec["dtype"] == "i32" else 1
+    esz = 4 if dcode == 0 else 8
+    seed = 1
+    kind = spec["kind"]
+
+    # ---------------------------------------------------------- inputs
+    if kind == "sharded":
+        n = spec["n"]
+        lo, hi = n * rank // world, n * (rank + 1) // world
+        src = torch.empty(hi - lo, dtype=tdt, device=dev)
+        gen(L, dcode, DIST[spec["dist"]], src, seed, lo, n)
+        units = n
+        unit_bytes = 2 * esz
+        step = lambda: vx.sharded_sort(src, seed=seed)  # noqa: E731
+    elif kind == "sort":
+        n = spec["n"]
+        src = torch.empty(n, dtype=tdt, device=dev)
+        gen(L, dcode, DIST[spec["dist"]], src, seed, 0, n)
+        out = torch.empty_like(src)
+        units = n * world
+        unit_bytes = 2 * esz
+        step = lambda: vx.sort_into(src, out)  # noqa: E731
+    elif kind == "kv":
+        n = spec["n"]
+        src = torch.empty(n, dtype=tdt, device=dev)
+        vals = torch.empty(n, dtype=tdt, device=dev)
+        gen(L, dcode, DIST["u31"], src, seed, 0, n)
+        gen(L, dcode, DIST["index"], vals, seed, 0, n)
+        out, outv = torch.empty_like(src), torch.empty_like(vals)
+        units = n * world
+        unit_bytes = 2 * 2 * esz
+        step = lambda: vx.sort_into(src, out, values=vals, out_values=outv)  # noqa: E731
+    elif kind == "partition":
+        n = spec["n"]
+        src = torch.empty(n, dtype=tdt, device=dev)
+        gen(L, dcode, DIST["normal"], src, seed, 0, n)
+        pivot = float(src[vx.select_pivot(src, 0, n - 1)].item())
+        out = torch.empty_like(src)
+        units = n * world
+        unit_bytes = 2 * esz
+        step = lambda: vx.partition_region(src, pivot, out=out)  # noqa: E731
+    elif kind == "segments":
+        import inputs
+
+        nseg = spec["nseg"]
+        offs_np, vals_np = inputs.c2_input(np.int32 if dcode == 0 else np.float64, nseg=nseg)
+        offs = torch.from_numpy(offs_np).to(dev)
+        src = torch.from_numpy(vals_np).to(dev)
+        n = len(vals_np)
+        units = n * world
+        unit_bytes = 2 * esz  # + 8 B per offset, added below
+        step = lambda: vx.sort_segments(src, offs, validate=False)  # noqa: E731
+    torch.cuda.synchronize()
+
+    # ---------------------------------------------------------- warm-up
+    for _ in range(args.warmup):
+        r = step()
+        del r
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------------------------------------------------- timed
+    stream = torch.cuda.current_stream()
+    L.vx_profile_reset()
+    L.vx_profile_enable(1)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            r = step()
+            del r
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    L.vx_profile_enable(0)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = allmax(ms)
+    launches, kms, kel = prof_read(L)
+    value = units * args.steps / (ms_max / 1e3) / 1e9
+
+    # dominant kernel roofline
+    peak, peak_src = peaks()
+    dom = max(range(len(CLASSES)), key=lambda i: kms[i])
+    per_elem = unit_bytes
+    alg_bytes = per_elem * kel[dom]
+    if kind == "segments" and CLASSES[dom] == "segsort":
+        alg_bytes = per_elem * n * args.steps + 8 * (len(offs)) * args.steps
+    achieved = alg_bytes / (kms[dom] / 1e3) / 1e9 if kms[dom] > 0 else 0.0
+    roof = {"bound": "hbm", "kernel": CLASSES[dom], "achieved": round(achieved, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(CLASSES[dom]),
+            "peak_source": peak_src,
+            "alg_bytes_per_launch": int(alg_bytes / max(launches[dom], 1)),
+            "avg_launch_ms": round(kms[dom] / max(launches[dom], 1), 4)}
+    # whole-step roofline: one read+write pass at HBM peak (+ NVLink term)
+    step_bytes = unit_bytes * units / world
+    t_roof = step_bytes / (peak * 1e9)
+    if kind == "sharded" and world > 1:
+        t_roof += (units / world * esz * (world - 1) / world) / (NVL_GBS * 1e9)
+    kernels = {CLASSES[i]: {"launches": launches[i], "ms": round(kms[i], 3), "elems": kel[i]}
+               for i in range(len(CLASSES)) if launches[i]}
+    res = dict(value=value, ms=ms_max / args.steps, roofline=roof, kernels=kernels,
+               step_roofline={"t_roof_ms": round(t_roof * 1e3, 4),
+                              "frac": round(t_roof * 1e3 / (ms_max / args.steps), 4),
+                              "passes_equiv": round((ms_max / args.steps) / (t_roof * 1e3), 2)},
+               gpu_launches=int(sum(launches)), clocks=clk.summary(), units=units)
+
+    # ---------------------------------------------------------- e2e
+    if not args.no_e2e:
+        extra = {}
+        if kind == "segments":
+            extra["offs_host"] = torch.from_numpy(offs_np).pin_memory()
+        res["e2e"] = run_e2e(args, spec, vx, L, src, vals if kind == "kv" else None, dev, rank, world, units,
+                             extra)
+    # ---------------------------------------------------------- cpu baseline
+    if rank == 0 and world == 1 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(spec, args, src=src)
+    return res
+
+
+def run_e2e(args, spec, vx, L, src, vals, dev, rank, world, units, extra):
+    """Host buffers in, host buffers out, copies inside the timed region."""
+    import torch
+
+    kind = spec["kind"]
+    host = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+    hv = torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True) if (kind == "kv") else None
+    code = 0 if src.dtype == torch.int32 else 1
+    times = []
+    h2d = src.numel() * src.element_size() * (2 if hv is not None else 1)
+    if "offs_host" in extra:
+        h2d += extra["offs_host"].numel() * 8
+    d2h = h2d
+    torch.cuda.empty_cache()
+    for it in range(args.warmup + args.steps):
+        host.copy_(src)  # restore pristine input (untimed)
+        if hv is not None:
+            hv.copy_(vals)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        if kind == "sort" and world == 1:
+            # reference-facing C ABI, host buffers (twin of _kernels.quicksort)
+            rc = L.vx_host_quicksort(code, ctypes.c_void_p(host.data_ptr()), host.numel(), 16 if code == 0 else 8,
+                                     0, 0, 0, 0, 0)
+            assert rc == 0, L.vx_last_error()
+        elif kind == "kv" and world == 1:
+            rc = L.vx_host_kv_quicksort(code, ctypes.c_void_p(host.data_ptr()), ctypes.c_void_p(hv.data_ptr()),
+                                        host.numel(), 16 if code == 0 else 8, 0, 0, 0, 0, 0)
+            assert rc == 0, L.vx_last_error()
+        elif kind == "partition":
+            pc = ctypes.c_double(float(src[vx.select_pivot(src, 0, src.numel() - 1)].item()))
+            b = L.vx_host_partition(1, ctypes.c_void_p(host.data_ptr()), 0, host.numel(), ctypes.byref(pc), 8, 0, 0)
+            assert b >= 0
+        elif kind == "sharded" and world == 1:
+            rc = L.vx_host_quicksort(code, ctypes.c_void_p(host.data_ptr()), host.numel(), 16 if code == 0 else 8,
+                                     0, 0, 0, 0, 0)
+            assert rc == 0, L.vx_last_error()
+        else:
+            # public Python API: pinned host -> device -> sort -> pinned host
+            d = host.to(dev, non_blocking=True)
+            if kind == "sharded":
+                out = vx.sharded_sort(d)
+                res_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+                res_h.copy_(out, non_blocking=True)
+                d2h = out.numel() * out.element_size()
+            else:  # segments, in place: offsets travel with the values
+                offs = extra["offs_host"].to(dev, non_blocking=True)
+                vx.sort_segments(d, offs, validate=False)
+                host.copy_(d, non_blocking=True)
+            torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        if it >= args.warmup:
+            times.append(t1 - t0)
+    total = allmax(sum(times))
+    L.vx_host_release()
+    return {"value": units * args.steps / total / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(total / args.steps * 1e3, 3),
+            "path": "vx_host_* C ABI (host buffers)" if world == 1 and kind != "segments" else
+            "public API, pinned host tensors"}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_sample(spec, src=None, n_sample=None):
+    """A bounded sample of the same workload on the host (numpy)."""
+    import numpy as np
+
+    import inputs
+
+    kind = spec["kind"]
+    if kind in ("sort", "sharded"):
+        n = n_sample or (1 << 24)
+        if src is not None:
+            return src[:n].cpu().numpy().copy(), f"first 2^{n.bit_length()-1} elements of the device input"
+        dt = np.int32 if spec["dtype"] == "i32" else np.float64
+        return inputs.c5_input(dt, spec["dist"], n=n * 64 // 64), f"2^{n.bit_length()-1}-element C5 input"
+    if kind == "kv":
+        n = n_sample or (1 << 22)
+        k, v = inputs.c4_input(n=n)
+        return (k, v), f"2^{n.bit_length()-1} C4 pairs"
+    if kind == "partition":
+        n = n_sample or (1 << 26)
+        return inputs.c3_input(n=n), f"2^{n.bit_length()-1} C3 normals"
+    if kind == "segments":
+        nseg = n_sample or (1 << 16)
+        dt = np.int32 if spec["dtype"] == "i32" else np.float64
+        return inputs.c2_input(dt, nseg=nseg), f"2^{nseg.bit_length()-1} C2 segments"
+
+
+def cpu_run_once(spec, sample, nthreads):
+    """Run the oracle port once on a fresh copy; return (elements, seconds)."""
+    import oracle
+
+    kind = spec["kind"]
+    if kind in ("sort", "sharded"):
+        a = sample.copy()
+        t0 = time.perf_counter()
+        oracle.sort(a, nthreads=nthreads)
+        return len(a), time.perf_counter() - t0
+    if kind == "kv":
+        k, v = sample[0].copy(), sample[1].copy()
+        t0 = time.perf_counter()
+        oracle.kv_sort(k, v, nthreads=nthreads)
+        return len(k), time.perf_counter() - t0
+    if kind == "partition":
+        a = sample.copy()
+        p = a[oracle.median3_index(a, 0, len(a) - 1)]
+        t0 = time.perf_counter()
+        oracle.partition_region(a, p)
+        return len(a), time.perf_counter() - t0
+    if kind == "segments":
+        offs, vals = sample
+        a = vals.copy()
+        sent = oracle.sentinel_for(a)
+        t0 = time.perf_counter()
+        for s in range(len(offs) - 1):
+            oracle.smallsort_region(a, int(offs[s]), int(offs[s + 1] - offs[s]), sent)
+        return len(a), time.perf_counter() - t0
+
+
+def cpu_threads(spec):
+    import oracle
+
+    # partition / small sorts are single-threaded in the reference and the port
+    return oracle.max_threads() if spec["kind"] in ("sort", "sharded", "kv") else 1
+
+
+def cpu_baseline(spec, args, src=None):
+    sample, desc = cpu_sample(spec, src)
+    nt = cpu_threads(spec)
+    cpu_run_once(spec, sample, nt)  # warm (page faults, thread pool)
+    n, sec = cpu_run_once(spec, sample, nt)
+    return {"value": n / sec / 1e9, "unit": "Gelem/s", "cores": nt, "kind": "port",
+            "sample": f"{desc}; C port of _kernels.py (oracle/), "
+                      f"{'OpenMP task-parallel quicksort' if nt > 1 else 'single thread'}, {sec:.2f} s"}
+
+
+def run_reference(args, spec, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port) on the
+    host cores, rank 0 only; each step one bounded sample."""
+    if rank != 0:
+        return None
+    sample, desc = cpu_sample(spec)
+    nt = cpu_threads(spec)
+    for _ in range(args.warmup):
+        cpu_run_once(spec, sample, nt)
+    tot_n, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        n, s = cpu_run_once(spec, sample, nt)
+        tot_n += n
+        tot_s += s
+    v = tot_n / tot_s / 1e9
+    return {"value": v, "ms": tot_s / args.steps * 1e3,
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": nt, "kind": "port",
+                             "sample": f"{desc} per step; C port of _kernels.py (oracle/)"},
+            "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c5_i32_uniform")
+    ap.add_argument("--n", type=lambda s: int(eval(s, {}, {})), default=None, help="global n (e.g. 2**28)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    spec = workload_spec(args.workload, args.n)
+    dtype = {"i32": "int32", "f64": "float64"}[spec["dtype"]]
+    cfg = {"workload": args.workload, **{k: v for k, v in spec.items() if k not in ("kind", "scaling")}}
+    base = {"metric": METRIC, "unit": "Gelem/s", "higher_is_better": True, "scaling": spec["scaling"],
+            "vs_baseline": None, "dtype": dtype, "steps": args.steps, "warmup": args.warmup}
+
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        r = run_reference(args, spec, rank)
+        if r is None:
+            return
+        cfg["sample"] = r["cpu_baseline"]["sample"]
+        line = {**base, "impl": "reference", "value": r["value"], "n_gpus": args.gpus,
+                "ms_per_step": r["ms"], "data": "synthetic (seeded numpy generators, tests/golden/inputs.py)",
+                "config": cfg, "cpu_baseline": r["cpu_baseline"], "e2e": r["e2e"]}
+        print(json.dumps(line))
+        return
+
+    rank, world, local = dist_setup(args.gpus)
+    r = run_ours(args, spec, rank, world, local)
+    cfg["parallelism"] = (f"sample sort over {world} rank(s) (NCCL all-to-all)" if spec["kind"] == "sharded"
+                          else ("replicas" if world > 1 else "single GPU"))
+    cfg["l2"] = "inputs larger than the 126 MB L2 (no flush needed)" if r["units"] * 4 > (256 << 20) \
+        else "input fits in L2; steps re-run on resident data"
+    if rank == 0:
+        line = {**base, "value": r["value"], "n_gpus": world, "ms_per_step": r["ms"],
+                "data": "synthetic (device counter-hash generator, seed 1)", "config": cfg,
+                "roofline": r["roofline"], "step_roofline": r["step_roofline"], "kernels": r["kernels"],
+                "gpu_launches": r["gpu_launches"], "clocks": r["clocks"]}
+        if "e2e" in r:
+            line["e2e"] = r["e2e"]
+        if "cpu_baseline" in r:
+            line["cpu_baseline"] = r["cpu_baseline"]
+        print(json.dumps(line))
+    import torch.distributed as dist
+
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

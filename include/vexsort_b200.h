@@ -75,6 +75,11 @@ int vx_version(void);
 size_t vx_sort_workspace_bytes(int dtype, int has_values, int64_t n);
 int vx_sort(int dtype, void *keys, void *values, int64_t n, const vx_sort_config *cfg, void *ws,
             size_t ws_bytes, vx_stream_t stream);
+/* Out-of-place twin: sorted copy of in[n] into out[n]; the input is only
+ * read (by the first partition level), so it costs no extra traffic.
+ * in == out is the in-place vx_sort. */
+int vx_sort_into(int dtype, const void *in_keys, const void *in_values, void *out_keys, void *out_values,
+                 int64_t n, const vx_sort_config *cfg, void *ws, size_t ws_bytes, vx_stream_t stream);
 
 /* Pivot partition, out of place: out[0:split) <= pivot < out[split:n).
  * *pivot points to a HOST scalar of the key type.  The split (= count of
@@ -114,6 +119,16 @@ int vx_select_splitters(int dtype, const void *d_sample_keys, const uint64_t *d_
  * 6 index (values = global index). */
 int vx_generate(int dtype, int dist, void *out, int64_t n, uint64_t seed, uint64_t global_offset,
                 int64_t global_n, vx_stream_t stream);
+
+/* Instrumentation.  Kernel launches are always counted per class; with
+ * profiling enabled every launch is also bracketed by CUDA events on its
+ * stream.  Classes: 0 plan, 1 hist, 2 emit, 3 scatter, 4 finish,
+ * 5 partition, 6 segsort, 7 bucket-partition.  vx_profile_read fills up to
+ * nclass entries (launch counts, summed device ms, elements processed) and
+ * returns the number of classes. */
+int vx_profile_enable(int on);
+int vx_profile_reset(void);
+int vx_profile_read(int64_t *launches, double *ms, uint64_t *elems, int nclass);
 
 /* ------------------------------------------------------- host-buffer drop-in */
 /* Same argument order as the _kernels.py functions they replace.  Arrays are

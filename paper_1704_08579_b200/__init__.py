@@ -30,7 +30,7 @@ from .lanes import (
     native_available,
 )
 from .partition import partition_region, scalar_partition
-from .quicksort import SortConfig, select_pivot, sort, sort_with_config
+from .quicksort import SortConfig, select_pivot, sort, sort_into, sort_with_config
 from .sharded import sharded_sort
 from .smallsort import sort_segments, sort_small_region
 
@@ -39,6 +39,7 @@ __version__ = "0.1.0"
 __all__ = [
     "sort",
     "sort_with_config",
+    "sort_into",
     "SortConfig",
     "select_pivot",
     "partition_region",

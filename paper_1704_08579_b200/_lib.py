@@ -49,6 +49,11 @@ def _declare(L):
         "vx_version": ([], i32),
         "vx_sort_workspace_bytes": ([i32, i32, i64], sz),
         "vx_sort": ([i32, vp, vp, i64, ctypes.POINTER(SortConfigC), vp, sz, vp], i32),
+        "vx_sort_into": ([i32, vp, vp, vp, vp, i64, ctypes.POINTER(SortConfigC), vp, sz, vp], i32),
+        "vx_profile_enable": ([i32], i32),
+        "vx_profile_reset": ([], i32),
+        "vx_profile_read": ([ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double),
+                             ctypes.POINTER(ctypes.c_uint64), i32], i32),
         "vx_partition_workspace_bytes": ([i32, i64], sz),
         "vx_partition": ([i32, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp], i32),
         "vx_sort_segments": ([i32, vp, vp, vp, i64, vp, sz, vp], i32),

@@ -71,7 +71,8 @@ struct Ctl {
     unsigned nseg;      // segments in this level's queue
     unsigned spl_ctr, bkt_ctr, tile_ctr, fin_ctr;
     unsigned err;
-    unsigned pad[2];
+    unsigned long long scat_elems;  // elements moved by this level's scatter
+    unsigned long long fin_elems;   // elements finished (sorted / copied) at this level
 };
 enum : unsigned { kErrCapacity = 1, kErrTooLong = 2 };
 
@@ -407,7 +408,7 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
 template <typename K, typename V>
 __global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v,
-                                                           const Seg* __restrict__ segs, const Ctl* __restrict__ ctl,
+                                                           const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
                                                            const unsigned* __restrict__ tile_owner,
                                                            const K* __restrict__ spl_pool,
                                                            unsigned long long* __restrict__ bkt_pool) {
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__
         __syncthreads();
         const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
         const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
+        if (threadIdx.x == 0) atomicAdd(&ctl->scat_elems, (unsigned long long)tn);
         K k[IPT];
         V v[IPT];
         unsigned bk[IPT];
@@ -573,7 +575,7 @@ __device__ void fin_local_sort(FinSmem<K, V>& sm, const K* src_k, const V* src_v
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, const Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, Ctl* __restrict__ ctl,
                                                            K* __restrict__ data_k, V* __restrict__ data_v,
                                                            const K* __restrict__ scr_k, const V* __restrict__ scr_v,
                                                            uint64_t seed, unsigned leaf) {
@@ -583,6 +585,7 @@ __global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict
     const unsigned nf = ctl->fin_ctr;
     for (unsigned d = blockIdx.x; d < nf; d += gridDim.x) {
         const Fin f = fins[d];
+        if (threadIdx.x == 0) atomicAdd(&ctl->fin_elems, (unsigned long long)f.len);
         const K* sk = (f.flags & 1u) ? scr_k : data_k;
         const V* sv = (f.flags & 1u) ? scr_v : data_v;
         if (f.flags & 2u) {

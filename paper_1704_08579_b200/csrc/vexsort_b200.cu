@@ -8,6 +8,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/vexsort_b200.h"
 #include "common.cuh"
@@ -92,19 +93,88 @@ struct SortLayout {
 };
 
 struct PinnedScratch {
-    unsigned* p = nullptr;
-    unsigned* get() {
-        if (!p) cudaHostAlloc((void**)&p, 64, cudaHostAllocDefault);
+    unsigned long long* p = nullptr;
+    unsigned long long* get() {
+        if (!p) cudaHostAlloc((void**)&p, 256, cudaHostAllocDefault);
         return p;
     }
 };
 thread_local PinnedScratch g_pinned;
 
+// ----------------------------------------------------------- instrumentation
+// Launch counting is always on; per-launch CUDA-event timing is opt-in
+// (vx_profile_enable) and brackets each kernel on its own stream.
+enum KClass { KC_PLAN = 0, KC_HIST, KC_EMIT, KC_SCATTER, KC_FINISH, KC_PARTITION, KC_SEGSORT, KC_BUCKET, KC_N };
+struct KProf {
+    std::mutex mu;
+    bool on = false;
+    long long launches[KC_N] = {};
+    double ms[KC_N] = {};
+    unsigned long long elems[KC_N] = {};
+    struct Pending { int cls; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> pool;
+    cudaEvent_t ev() {
+        if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+KProf g_prof;
+
+struct Launch {  // RAII bracket: count the launch, optionally time it
+    int cls;
+    cudaStream_t st;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Launch(int c, cudaStream_t s, int count = 1) : cls(c), st(s) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.launches[cls] += count;
+        if (g_prof.on) {
+            a = g_prof.ev();
+            b = g_prof.ev();
+            cudaEventRecord(a, st);
+        }
+    }
+    ~Launch() {
+        if (a) {
+            cudaEventRecord(b, st);
+            std::lock_guard<std::mutex> lk(g_prof.mu);
+            g_prof.pending.push_back({cls, a, b});
+        }
+    }
+};
+
+void prof_collect() {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto& p : g_prof.pending) {
+        cudaEventSynchronize(p.b);
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) g_prof.ms[p.cls] += t;
+        g_prof.pool.push_back(p.a);
+        g_prof.pool.push_back(p.b);
+    }
+    g_prof.pending.clear();
+}
+void prof_elems(int cls, unsigned long long e) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.elems[cls] += e;
+}
+
+// in_k may equal out_k (in place).  Level 0 reads the input; every later
+// level and the finish kernels work in out / scratch only, so an
+// out-of-place sort leaves the input untouched at no extra traffic.
 template <typename K, typename V>
-int run_sort(K* keys, V* vals, uint64_t n, const vx_sort_config* cfg, void* ws, size_t ws_bytes,
-             cudaStream_t st) {
+int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const vx_sort_config* cfg, void* ws,
+             size_t ws_bytes, cudaStream_t st) {
     using L = SortLayout<K, V>;
-    if (n < 2) return VX_OK;
+    if (n < 2) {
+        if (n == 1 && in_k != keys) {
+            VX_CUDA(cudaMemcpyAsync(keys, in_k, sizeof(K), cudaMemcpyDeviceToDevice, st));
+            if (HasVal<V>::value) VX_CUDA(cudaMemcpyAsync(vals, in_v, sizeof(V), cudaMemcpyDeviceToDevice, st));
+        }
+        return VX_OK;
+    }
     L lay(n);
     if (ws_bytes < lay.total || !ws) return fail(VX_EWORKSPACE, "sort workspace too small");
     const int lanes = sizeof(K) == 4 ? 16 : 8;
@@ -130,54 +200,79 @@ int run_sort(K* keys, V* vals, uint64_t n, const vx_sort_config* cfg, void* ws, 
     const int g_hist = sms * occ_hist, g_scat = sms * occ_scat, g_fin = sms * occ_fin;
 
     VX_CUDA(cudaMemsetAsync(ctl, 0, kMaxLevels * sizeof(Ctl), st));
+    unsigned long long* hp = g_pinned.get();
+    if (!hp) return fail(VX_ECUDA, "cudaHostAlloc failed");
     if (n <= L::LOCAL) {
-        // whole array is one finish item (in place)
-        Fin f{0ull, (unsigned)n, 0u};
+        // the whole array is one finish item; its source is the input
+        Fin f{0ull, (unsigned)n, in_k == keys ? 0u : 1u};
         VX_CUDA(cudaMemcpyAsync(fins, &f, sizeof(Fin), cudaMemcpyHostToDevice, st));
         unsigned one = 1;
         VX_CUDA(cudaMemcpyAsync(&ctl[0].fin_ctr, &one, sizeof(unsigned), cudaMemcpyHostToDevice, st));
-        qs_finish_kernel<K, V><<<1, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, ctl, keys, vals, sk, sv, seed,
-                                                                         (unsigned)bound);
+        {
+            Launch l(KC_FINISH, st);
+            qs_finish_kernel<K, V><<<1, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, ctl, keys, vals, in_k, in_v, seed,
+                                                                             (unsigned)bound);
+        }
         VX_LAUNCHED();
+        if (g_prof.on) prof_elems(KC_FINISH, n);
         return VX_OK;
     }
     qs_init_kernel<<<1, 1, 0, st>>>(segs[0], ctl, n);
     VX_LAUNCHED();
-    unsigned* hp = g_pinned.get();
-    if (!hp) return fail(VX_ECUDA, "cudaHostAlloc failed");
     unsigned nseg = 1;
     for (int level = 0; level < kMaxLevels - 1; ++level) {
         const bool even = (level & 1) == 0;
-        const K* src_k = even ? keys : sk;
-        const V* src_v = even ? vals : sv;
+        const K* src_k = level == 0 ? in_k : (even ? keys : sk);
+        const V* src_v = level == 0 ? in_v : (even ? vals : sv);
         K* dst_k = even ? sk : keys;
         V* dst_v = even ? sv : vals;
         Ctl* c = ctl + level;
         const uint64_t lvl_seed = mix64(seed + 0x51ED270B27AD1CULL * (level + 1));
         const unsigned g_seg = std::min<unsigned>(nseg, (unsigned)sms * 4);
-        qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, segs[level & 1], c, spl, bkt, towner,
-                                                         (unsigned)lay.cap_spl, (unsigned)lay.cap_bkt,
-                                                         (unsigned)lay.cap_tiles, lvl_seed);
+        {
+            Launch l(KC_PLAN, st);
+            qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, segs[level & 1], c, spl, bkt, towner,
+                                                             (unsigned)lay.cap_spl, (unsigned)lay.cap_bkt,
+                                                             (unsigned)lay.cap_tiles, lvl_seed);
+        }
         VX_LAUNCHED();
-        qs_hist_kernel<K><<<g_hist, kQsNT, 0, st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
+        {
+            Launch l(KC_HIST, st);
+            qs_hist_kernel<K><<<g_hist, kQsNT, 0, st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
+        }
         VX_LAUNCHED();
-        qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
-                                                         segs[(level + 1) & 1], bkt, fins,
-                                                         (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
-                                                         even ? 1 : 0);
+        {
+            Launch l(KC_EMIT, st);
+            qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
+                                                             segs[(level + 1) & 1], bkt, fins,
+                                                             (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
+                                                             even ? 1 : 0);
+        }
         VX_LAUNCHED();
-        qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterSmem<K, V>), st>>>(
-            src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
+        {
+            Launch l(KC_SCATTER, st);
+            qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterSmem<K, V>), st>>>(
+                src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
+        }
         VX_LAUNCHED();
-        qs_finish_kernel<K, V><<<g_fin, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, c, keys, vals, sk, sv,
-                                                                            lvl_seed, (unsigned)bound);
+        {
+            Launch l(KC_FINISH, st);
+            qs_finish_kernel<K, V><<<g_fin, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, c, keys, vals, sk, sv,
+                                                                                lvl_seed, (unsigned)bound);
+        }
         VX_LAUNCHED();
-        // queue size of the next level (and error flags) back to the host
+        // next level's queue size, error flags and element counters -> host
         VX_CUDA(cudaMemcpyAsync(hp, &ctl[level + 1].nseg, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaMemcpyAsync(hp + 1, &c->err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        VX_CUDA(cudaMemcpyAsync(hp + 2, &c->scat_elems, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaStreamSynchronize(st));
-        if (hp[1]) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
-        nseg = hp[0];
+        if (g_prof.on) {
+            prof_elems(KC_SCATTER, hp[2]);
+            prof_elems(KC_FINISH, hp[3]);
+            prof_collect();
+        }
+        if ((unsigned)hp[1]) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
+        nseg = (unsigned)hp[0];
         if (nseg == 0) return VX_OK;
     }
     return fail(VX_ECAPACITY, "sort exceeded the maximum level count");
@@ -205,6 +300,8 @@ int run_partition(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, K pi
     const size_t smem = (size_t)T * (sizeof(K) + (KV ? sizeof(V) : 0));
     const bool vec = ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(vin)) & 15) == 0;
     auto* ds = reinterpret_cast<unsigned long long*>(d_split);
+    Launch lch(KC_PARTITION, st);
+    if (g_prof.on) prof_elems(KC_PARTITION, n);
     if (vec) {
         static int o1 = prepare(partition2_kernel<K, V, NT, IPT, true>, NT, smem);
         (void)o1;
@@ -367,14 +464,56 @@ int vx_sort(int dtype, void* keys, void* values, int64_t n, const vx_sort_config
             vx_stream_t stream) {
     if (int rc = check_dtype(dtype)) return rc;
     if (n < 0 || (n > 0 && !keys)) return fail(VX_EINVAL, "bad array");
+    return vx_sort_into(dtype, keys, values, keys, values, n, cfg, ws, ws_bytes, stream);
+}
+
+int vx_sort_into(int dtype, const void* in_keys, const void* in_values, void* out_keys, void* out_values, int64_t n,
+                 const vx_sort_config* cfg, void* ws, size_t ws_bytes, vx_stream_t stream) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n < 0 || (n > 0 && (!in_keys || !out_keys))) return fail(VX_EINVAL, "bad array");
+    if ((in_values == nullptr) != (out_values == nullptr)) return fail(VX_EINVAL, "values in/out mismatch");
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == VX_I32) {
-        if (values)
-            return run_sort<int32_t, uint32_t>((int32_t*)keys, (uint32_t*)values, n, cfg, ws, ws_bytes, st);
-        return run_sort<int32_t, NoVal>((int32_t*)keys, nullptr, n, cfg, ws, ws_bytes, st);
+        if (in_values)
+            return run_sort<int32_t, uint32_t>((const int32_t*)in_keys, (const uint32_t*)in_values, (int32_t*)out_keys,
+                                               (uint32_t*)out_values, n, cfg, ws, ws_bytes, st);
+        return run_sort<int32_t, NoVal>((const int32_t*)in_keys, nullptr, (int32_t*)out_keys, nullptr, n, cfg, ws,
+                                        ws_bytes, st);
     }
-    if (values) return run_sort<double, uint64_t>((double*)keys, (uint64_t*)values, n, cfg, ws, ws_bytes, st);
-    return run_sort<double, NoVal>((double*)keys, nullptr, n, cfg, ws, ws_bytes, st);
+    if (in_values)
+        return run_sort<double, uint64_t>((const double*)in_keys, (const uint64_t*)in_values, (double*)out_keys,
+                                          (uint64_t*)out_values, n, cfg, ws, ws_bytes, st);
+    return run_sort<double, NoVal>((const double*)in_keys, nullptr, (double*)out_keys, nullptr, n, cfg, ws, ws_bytes,
+                                   st);
+}
+
+int vx_profile_enable(int on) {
+    prof_collect();
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    return VX_OK;
+}
+
+int vx_profile_reset(void) {
+    prof_collect();
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (int i = 0; i < KC_N; ++i) {
+        g_prof.launches[i] = 0;
+        g_prof.ms[i] = 0.0;
+        g_prof.elems[i] = 0;
+    }
+    return VX_OK;
+}
+
+int vx_profile_read(int64_t* launches, double* ms, uint64_t* elems, int nclass) {
+    prof_collect();
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (int i = 0; i < nclass && i < KC_N; ++i) {
+        if (launches) launches[i] = g_prof.launches[i];
+        if (ms) ms[i] = g_prof.ms[i];
+        if (elems) elems[i] = g_prof.elems[i];
+    }
+    return KC_N;
 }
 
 size_t vx_partition_workspace_bytes(int dtype, int64_t n) {
@@ -417,6 +556,7 @@ int vx_sort_segments(int dtype, void* keys, void* values, const int64_t* d_offse
     const unsigned grid = (unsigned)std::min<int64_t>((nseg + 7) / 8, (int64_t)num_sms() * 16);
     auto* err = static_cast<unsigned*>(ws);
     const auto* offs = reinterpret_cast<const long long*>(d_offsets);
+    Launch lch(KC_SEGSORT, st);
     if (dtype == VX_I32) {
         if (values) segsort_kernel<int32_t, uint32_t><<<grid, 256, 0, st>>>((int32_t*)keys, (uint32_t*)values, offs, nseg, err);
         else segsort_kernel<int32_t, NoVal><<<grid, 256, 0, st>>>((int32_t*)keys, nullptr, offs, nseg, err);
@@ -452,6 +592,8 @@ int vx_bucket_partition(int dtype, const void* in_keys, void* out_keys, int64_t 
     VX_CUDA(cudaMemsetAsync(d_counts, 0, (nsplit + 1) * 8, st));
     if (n == 0) return VX_OK;
     const int sms = num_sms();
+    Launch lch(KC_BUCKET, st, 3);
+    if (g_prof.on) prof_elems(KC_BUCKET, n);
     if (dtype == VX_I32) {
         using K = int32_t;
         static int occ = prepare(bp_scatter_kernel<K, NoVal>, kQsNT, sizeof(ScatterSmem<K, NoVal>));

@@ -16,7 +16,7 @@ from ._lib import SortConfigC, check, lib
 from ._region import check_region, dev_ptr, host_ptr, stream_of, workspace
 from .lanes import get_backend, is_device
 
-__all__ = ["SortConfig", "sort", "sort_with_config", "select_pivot", "MAX_PACKS"]
+__all__ = ["SortConfig", "sort", "sort_with_config", "sort_into", "select_pivot", "MAX_PACKS"]
 
 MAX_PACKS = 16  # smallsort.py:40
 _PIVOT_STRATEGIES = ("median3", "middle", "random")
@@ -95,6 +95,26 @@ def sort_with_config(region, config: SortConfig) -> None:
     check(L.vx_host_quicksort(kind.code, host_ptr(region), n, backend.lanes, bound,
                               _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),
                               int(config.swap_buffered), int(config.pivot_seed) & _U64), "sort")
+
+
+def sort_into(src, out, config: SortConfig | None = None, values=None, out_values=None):
+    """Device-only out-of-place sort: out = sorted(src) (pairs with values /
+    out_values).  src is only read, by the first partition level, so this
+    costs the same HBM traffic as the in-place sort."""
+    config = config or SortConfig()
+    kind = check_region(src)
+    assert is_device(src) and is_device(out) and out.dtype == src.dtype and len(out) == len(src)
+    assert out.is_contiguous()
+    n = len(src)
+    backend = get_backend(config.backend, kind)
+    bound = _resolve_bound(config, backend.lanes)
+    L = lib()
+    ws = workspace(L.vx_sort_workspace_bytes(kind.code, int(values is not None), n), src.device)
+    cfg = _cfg(config, bound)
+    check(L.vx_sort_into(kind.code, dev_ptr(src), dev_ptr(values) if values is not None else None, dev_ptr(out),
+                         dev_ptr(out_values) if out_values is not None else None, n, ctypes.byref(cfg),
+                         dev_ptr(ws), ws.numel(), stream_of(src)), "sort_into")
+    return out
 
 
 def sort(region, config: SortConfig | None = None) -> None:

@@ -28,7 +28,7 @@ from dataclasses import dataclass
 
 from ._lib import check, lib
 from ._region import check_region, dev_ptr, stream_of, workspace
-from .quicksort import SortConfig, sort_with_config
+from .quicksort import SortConfig, sort_into, sort_with_config
 
 __all__ = ["sharded_sort", "sample_positions", "B200Ops", "ExchangeStats"]
 
@@ -88,6 +88,11 @@ class B200Ops:
         sort_with_config(x, SortConfig(pivot_seed=seed))
         return x
 
+    def local_sort_into(self, x, seed):
+        import torch
+
+        return sort_into(x, torch.empty_like(x), SortConfig(pivot_seed=seed))
+
 
 def sharded_sort(local, group=None, *, samples_per_rank: int = 1024, seed: int = 0, ops=None,
                  stats: ExchangeStats | None = None):
@@ -104,7 +109,7 @@ def sharded_sort(local, group=None, *, samples_per_rank: int = 1024, seed: int =
     if stats is not None:
         stats.n_local_in = n_local
     if P == 1:
-        out = ops.local_sort(local, seed)
+        out = ops.local_sort_into(local, seed)
         if stats is not None:
             stats.n_local_out = n_local
             stats.send_counts = stats.recv_counts = [n_local]
