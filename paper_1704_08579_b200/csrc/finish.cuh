@@ -1,0 +1,255 @@
+// finish.cuh -- CTA-local hybrid quicksort of one small range (<= CAP
+// elements) and the finish queue kernel.
+//
+// This is the bottom of the reference's recursion (_kernels.py:396-423): a
+// range small enough for one SM is partitioned once more around sampled
+// pivots and every resulting range <= the leaf bound is sorted by the
+// bitonic network (_kernels.py:30-58, 97-113).  B200 shape, one HBM read and
+// one HBM write per element:
+//   * the range is loaded straight into registers (coalesced, striped);
+//   * one warp sorts a <= 512-element sample in registers (warp bitonic) and
+//     the CTA picks up to 63 distinct pivots -> 2m+1 buckets (ranges and
+//     equal-to-pivot buckets, the latter already final);
+//   * each element is classified once (branch-free search in smem), ranked
+//     with a shared-memory atomic, and written bucket-major into a padded
+//     smem buffer (one pad word per 32 makes blocked warp reads conflict-free);
+//   * warps sort the range buckets IN shared memory with the register
+//     bitonic network; buckets above the leaf bound are written out as they
+//     are and re-queued for another finish round (the reference's "partition
+//     again" branch);
+//   * the whole range, now sorted, leaves with one coalesced store.
+#pragma once
+
+#include "bitonic.cuh"
+#include "common.cuh"
+#include "qsort.cuh"
+
+namespace vx {
+
+constexpr int kFinMaxSplit = 63;
+constexpr int kFinMaxBkt = 2 * kFinMaxSplit + 1;
+constexpr int kFinMaxSample = 512;
+constexpr unsigned kWarpSortMax = 512;
+
+__device__ __forceinline__ unsigned pad32(unsigned i) { return i + (i >> 5); }
+
+template <typename K, typename V>
+struct FinSmem {
+    static constexpr uint32_t CAP = FinCap<K, V>::value;
+    static constexpr uint32_t PCAP = CAP + CAP / 32;
+    using VS = typename std::conditional<HasVal<V>::value, V, char>::type;
+    K b[PCAP];
+    VS bv[HasVal<V>::value ? PCAP : 1];
+    K samp[kFinMaxSample];
+    K spl[kFinMaxSplit + 1];
+    unsigned cnt[kFinMaxBkt + 1];
+    unsigned loc[kFinMaxBkt + 2];
+    unsigned scan[kFinNT / 32 + 1];
+};
+
+// Sort P = 32*E padded-smem slots b[pad32(lo + q)], q < c, in place with one
+// warp (blocked layout, sentinel padding by count).
+template <typename K, typename V, int E>
+__device__ __forceinline__ void warp_sort_smem_e(K* b, V* bv, unsigned lo, unsigned c) {
+    constexpr bool KV = HasVal<V>::value;
+    const unsigned lane = threadIdx.x & 31;
+    K k[E];
+    V v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const unsigned q = lane * E + r;
+        k[r] = q < c ? b[pad32(lo + q)] : KeyTraits<K>::sentinel();
+        if constexpr (KV) v[r] = q < c ? bv[pad32(lo + q)] : V();
+    }
+    WarpBitonic<K, V, E>::sort(k, v);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const unsigned q = lane * E + r;
+        if (q < c) {
+            b[pad32(lo + q)] = k[r];
+            if constexpr (KV) bv[pad32(lo + q)] = v[r];
+        }
+    }
+    __syncwarp();
+}
+
+template <typename K, typename V>
+__device__ __forceinline__ void warp_sort_smem(K* b, V* bv, unsigned lo, unsigned c) {
+    if (c <= 32) warp_sort_smem_e<K, V, 1>(b, bv, lo, c);
+    else if (c <= 64) warp_sort_smem_e<K, V, 2>(b, bv, lo, c);
+    else if (c <= 128) warp_sort_smem_e<K, V, 4>(b, bv, lo, c);
+    else if (c <= 256) warp_sort_smem_e<K, V, 8>(b, bv, lo, c);
+    else warp_sort_smem_e<K, V, 16>(b, bv, lo, c);
+}
+
+// sort the S (pow2, 32..512) samples of smem `s` ascending with one warp
+template <typename K>
+__device__ __forceinline__ void warp_sort_samples(K* s, unsigned S) {
+    // samples live unpadded: reuse the padded helper on a tiny view is not
+    // needed -- read blocked directly (S <= 512, a few bank conflicts)
+    const unsigned lane = threadIdx.x & 31;
+    auto run = [&](auto e_tag) {
+        constexpr int E = decltype(e_tag)::value;
+        K k[E];
+        NoVal v[E];
+#pragma unroll
+        for (int r = 0; r < E; ++r) k[r] = s[lane * E + r];
+        WarpBitonic<K, NoVal, E>::sort(k, v);
+#pragma unroll
+        for (int r = 0; r < E; ++r) s[lane * E + r] = k[r];
+    };
+    switch (S) {
+        case 32: run(std::integral_constant<int, 1>{}); break;
+        case 64: run(std::integral_constant<int, 2>{}); break;
+        case 128: run(std::integral_constant<int, 4>{}); break;
+        case 256: run(std::integral_constant<int, 8>{}); break;
+        default: run(std::integral_constant<int, 16>{}); break;
+    }
+    __syncwarp();
+}
+
+template <typename K, typename V>
+__device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const V* __restrict__ src_v,
+                          K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t start, unsigned len, uint64_t seed,
+                          unsigned leaf, Ctl* ctl, Ctl* ctl_next, Fin* fins_next, unsigned cap_fin) {
+    constexpr bool KV = HasVal<V>::value;
+    constexpr unsigned CAP = FinSmem<K, V>::CAP;
+    constexpr int IPT = CAP / kFinNT;
+    constexpr int NW = kFinNT / 32;
+    const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+    // 1. the range into registers, striped and coalesced
+    K x[IPT];
+    V y[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const unsigned p = j * kFinNT + tid;
+        if (p < len) {
+            x[j] = ld_stream(src_k + start + p);
+            if constexpr (KV) y[j] = ld_stream(src_v + start + p);
+        }
+    }
+    // 2. stratified sample (L1/L2-resident re-read), sorted by warp 0
+    const unsigned target = max(2u, min(128u, leaf / 2));
+    const unsigned mt = max(1u, min((unsigned)kFinMaxSplit, len / target));
+    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(8 * (mt + 1))));
+    if (tid < S) {
+        const unsigned stride = max(1u, len / S);
+        const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
+        const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
+        sm.samp[tid] = src_k[start + q];
+    }
+    __syncthreads();
+    if (warp == 0) warp_sort_samples<K>(sm.samp, S);
+    __syncthreads();
+    // 3. distinct pivots
+    K cand = K();
+    unsigned keep = 0;
+    if (tid < mt) {
+        const unsigned q = (unsigned)(((uint64_t)(tid + 1) * S) / (mt + 1));
+        cand = sm.samp[q];
+        keep = tid == 0 ? 1u : (sm.samp[(unsigned)(((uint64_t)tid * S) / (mt + 1))] < cand ? 1u : 0u);
+    }
+    unsigned m;
+    const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
+    const unsigned span = next_pow2_u32(m + 1);
+    const unsigned nb = 2 * m + 1;
+    if (keep) sm.spl[rank] = cand;
+    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<K>::sentinel();
+    if (tid < nb) sm.cnt[tid] = 0;
+    __syncthreads();
+    // 4. classify once, rank with smem atomics (bucket << 16 | rank)
+    unsigned br[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const unsigned p = j * kFinNT + tid;
+        if (p < len) {
+            const unsigned b = cls_eq(x[j], sm.spl, m, span);
+            br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
+        }
+    }
+    __syncthreads();
+    {
+        unsigned tot;
+        const unsigned c = tid < nb ? sm.cnt[tid] : 0u;
+        const unsigned ex = block_excl_scan<kFinNT>(c, sm.scan, &tot);
+        if (tid < nb) sm.loc[tid] = ex;
+        if (tid == 0) sm.loc[nb] = len;
+    }
+    __syncthreads();
+    // 5. bucket-major into the padded smem buffer
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const unsigned p = j * kFinNT + tid;
+        if (p < len) {
+            const unsigned slot = pad32(sm.loc[br[j] >> 16] + (br[j] & 0xffffu));
+            sm.b[slot] = x[j];
+            if constexpr (KV) sm.bv[slot] = y[j];
+        }
+    }
+    __syncthreads();
+    // 6. warps sort the range buckets in place; equal-to-pivot buckets are
+    //    final; oversize buckets are re-queued (written out unsorted below)
+    const unsigned wmax = min(leaf, kWarpSortMax);
+    for (unsigned b = 2 * warp; b < nb; b += 2 * NW) {
+        const unsigned lo = sm.loc[b], c = sm.loc[b + 1] - lo;
+        if (c < 2) continue;
+        if (c <= wmax) {
+            if constexpr (KV) warp_sort_smem<K, V>(sm.b, sm.bv, lo, c);
+            else warp_sort_smem<K, V>(sm.b, (V*)nullptr, lo, c);
+        } else if (lane == 0) {
+            const unsigned f = atomicAdd(&ctl_next->fin_ctr, 1u);
+            if (f < cap_fin) {
+                fins_next[f].start = start + lo;
+                fins_next[f].len = c;
+                fins_next[f].flags = 0u;  // next round sorts it in place in `data`
+            } else {
+                atomicOr(&ctl->err, kErrCapacity);
+            }
+        }
+    }
+    __syncthreads();
+    // 7. one coalesced store of the whole range
+    for (unsigned i = tid; i < len; i += kFinNT) {
+        dst_k[start + i] = sm.b[pad32(i)];
+        if constexpr (KV) dst_v[start + i] = sm.bv[pad32(i)];
+    }
+    __syncthreads();
+}
+
+// One CTA per finish item (grid-stride).  Items: copy (flags bit1), direct
+// warp bitonic (len <= leaf), or the CTA-local sort above.  Source is the
+// scratch buffer when flags bit0 is set, else `data` (in place).
+template <typename K, typename V>
+__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, Ctl* __restrict__ ctl,
+                                                           Ctl* __restrict__ ctl_next, Fin* __restrict__ fins_next,
+                                                           unsigned cap_fin, K* __restrict__ data_k,
+                                                           V* __restrict__ data_v, const K* __restrict__ scr_k,
+                                                           const V* __restrict__ scr_v, uint64_t seed,
+                                                           unsigned leaf) {
+    constexpr bool KV = HasVal<V>::value;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    FinSmem<K, V>& sm = *reinterpret_cast<FinSmem<K, V>*>(smem_raw);
+    const unsigned nf = ctl->fin_ctr;
+    const unsigned wmax = min(leaf, kWarpSortMax);
+    for (unsigned d = blockIdx.x; d < nf; d += gridDim.x) {
+        const Fin f = fins[d];
+        if (threadIdx.x == 0) atomicAdd(&ctl->fin_elems, (unsigned long long)f.len);
+        const K* sk = (f.flags & 1u) ? scr_k : data_k;
+        const V* sv = (f.flags & 1u) ? scr_v : data_v;
+        if (f.flags & 2u) {
+            for (unsigned i = threadIdx.x; i < f.len; i += kFinNT) {
+                data_k[f.start + i] = sk[f.start + i];
+                if constexpr (KV) data_v[f.start + i] = sv[f.start + i];
+            }
+        } else if (f.len <= min(wmax, 256u)) {
+            if (threadIdx.x < 32) warp_sort_any2<K, V>(sk + f.start, sv ? sv + f.start : nullptr, data_k + f.start,
+                                                       data_v ? data_v + f.start : nullptr, f.len);
+        } else {
+            fin_local<K, V>(sm, sk, sv, data_k, data_v, f.start, f.len, seed, leaf, ctl, ctl_next, fins_next,
+                            cap_fin);
+        }
+    }
+}
+
+}  // namespace vx

@@ -456,152 +456,6 @@ __global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__
     }
 }
 
-// ------------------------------------------------------------ finish
-template <typename K, typename V>
-struct FinSmem {
-    static constexpr uint32_t CAP = FinCap<K, V>::value;
-    K a[CAP];
-    K bb[CAP];
-    typename std::conditional<HasVal<V>::value, V, char>::type av[HasVal<V>::value ? CAP : 1];
-    typename std::conditional<HasVal<V>::value, V, char>::type bv[HasVal<V>::value ? CAP : 1];
-    K spl[256];
-    unsigned cnt[kMaxBkt + 1];
-    unsigned loc[kMaxBkt + 1];
-    unsigned scan[kFinNT / 32 + 1];
-};
-
-// CTA-local hybrid quicksort of one range (len <= CAP) from src into dst
-// (global), using shared memory as the working set.
-template <typename K, typename V>
-__device__ void fin_local_sort(FinSmem<K, V>& sm, const K* src_k, const V* src_v, K* dst_k, V* dst_v,
-                               uint64_t start, unsigned len, uint64_t seed, unsigned leaf) {
-    constexpr bool KV = HasVal<V>::value;
-    constexpr int NW = kFinNT / 32;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
-        sm.a[i] = src_k[start + i];
-        if constexpr (KV) sm.av[i] = src_v[start + i];
-    }
-    // sample into bb (free for now), sort it
-    unsigned S = next_pow2_u32(len / 8);
-    S = S < 256 ? 256 : (S > kFinSample ? kFinSample : S);
-    __syncthreads();
-    for (unsigned i = threadIdx.x; i < S; i += kFinNT) {
-        const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + i));
-        sm.bb[i] = sm.a[h % len];
-    }
-    __syncthreads();
-    cta_bitonic<K, NoVal, kFinNT>(sm.bb, nullptr, S);
-    unsigned mt = len / 96;
-    mt = mt < 2 ? 2 : (mt > 127 ? 127 : mt);
-    K cand = K();
-    unsigned keep = 0;
-    if (threadIdx.x < mt) {
-        const unsigned q = (unsigned)(((uint64_t)(threadIdx.x + 1) * S) / (mt + 1));
-        cand = sm.bb[q];
-        keep = threadIdx.x == 0 ? 1u
-                                : (sm.bb[(unsigned)(((uint64_t)threadIdx.x * S) / (mt + 1))] < cand ? 1u : 0u);
-    }
-    unsigned m;
-    const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
-    if (keep) sm.spl[rank] = cand;
-    const unsigned span = next_pow2_u32(m + 1);
-    const unsigned nb = 2 * m + 1;
-    __syncthreads();
-    for (unsigned i = m + threadIdx.x; i < span; i += kFinNT) sm.spl[i] = KeyTraits<K>::sentinel();
-    for (unsigned b = threadIdx.x; b < nb; b += kFinNT) sm.cnt[b] = 0;
-    __syncthreads();
-    // classify + rank (bucket id parked in bb as a temporary is not possible
-    // for K=int32 ranks, so recompute on the scatter pass)
-    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
-        const unsigned b = cls_eq(sm.a[i], sm.spl, m, span);
-        atomicAdd(&sm.cnt[b], 1u);
-    }
-    __syncthreads();
-    {
-        unsigned tot;
-        const unsigned c = threadIdx.x < nb ? sm.cnt[threadIdx.x] : 0u;
-        const unsigned ex = block_excl_scan<kFinNT>(c, sm.scan, &tot);
-        if (threadIdx.x < nb) {
-            sm.loc[threadIdx.x] = ex;
-            sm.cnt[threadIdx.x] = ex;  // becomes a running cursor
-        }
-    }
-    __syncthreads();
-    for (unsigned i = threadIdx.x; i < len; i += kFinNT) {
-        const K x = sm.a[i];
-        const unsigned b = cls_eq(x, sm.spl, m, span);
-        const unsigned slot = atomicAdd(&sm.cnt[b], 1u);
-        sm.bb[slot] = x;
-        if constexpr (KV) sm.bv[slot] = sm.av[i];
-    }
-    __syncthreads();
-    // every bucket: final -> copy; <= leaf -> warp bitonic; else below
-    for (unsigned b = warp; b < nb; b += NW) {
-        const unsigned lo = sm.loc[b], c = (b + 1 < nb ? sm.loc[b + 1] : len) - lo;
-        if (c == 0) continue;
-        if ((b & 1u) || c == 1) {
-            for (unsigned i = lane; i < c; i += 32) {
-                dst_k[start + lo + i] = sm.bb[lo + i];
-                if constexpr (KV) dst_v[start + lo + i] = sm.bv[lo + i];
-            }
-        } else if (c <= leaf) {
-            if constexpr (KV)
-                warp_sort_any2<K, V>(sm.bb + lo, sm.bv + lo, dst_k + start + lo, dst_v + start + lo, c);
-            else
-                warp_sort_any2<K, V>(sm.bb + lo, (const V*)nullptr, dst_k + start + lo, (V*)nullptr, c);
-        }
-    }
-    __syncthreads();
-    // rare: a range bucket above the leaf bound -> CTA bitonic in smem over a
-    // sentinel-padded copy in `a` (free by now; CAP is a power of two)
-    for (unsigned b = 0; b < nb; b += 2) {
-        const unsigned lo = sm.loc[b], c = (b + 1 < nb ? sm.loc[b + 1] : len) - lo;
-        if (c <= leaf) continue;
-        const unsigned P = next_pow2_u32(c);
-        for (unsigned i = threadIdx.x; i < P; i += kFinNT) {
-            sm.a[i] = i < c ? sm.bb[lo + i] : KeyTraits<K>::sentinel();
-            if constexpr (KV) sm.av[i] = i < c ? sm.bv[lo + i] : V();
-        }
-        __syncthreads();
-        if constexpr (KV) cta_bitonic<K, V, kFinNT>(sm.a, sm.av, P);
-        else cta_bitonic<K, NoVal, kFinNT>(sm.a, nullptr, P);
-        for (unsigned i = threadIdx.x; i < c; i += kFinNT) {
-            dst_k[start + lo + i] = sm.a[i];
-            if constexpr (KV) dst_v[start + lo + i] = sm.av[i];
-        }
-        __syncthreads();
-    }
-}
-
-template <typename K, typename V>
-__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, Ctl* __restrict__ ctl,
-                                                           K* __restrict__ data_k, V* __restrict__ data_v,
-                                                           const K* __restrict__ scr_k, const V* __restrict__ scr_v,
-                                                           uint64_t seed, unsigned leaf) {
-    constexpr bool KV = HasVal<V>::value;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    FinSmem<K, V>& sm = *reinterpret_cast<FinSmem<K, V>*>(smem_raw);
-    const unsigned nf = ctl->fin_ctr;
-    for (unsigned d = blockIdx.x; d < nf; d += gridDim.x) {
-        const Fin f = fins[d];
-        if (threadIdx.x == 0) atomicAdd(&ctl->fin_elems, (unsigned long long)f.len);
-        const K* sk = (f.flags & 1u) ? scr_k : data_k;
-        const V* sv = (f.flags & 1u) ? scr_v : data_v;
-        if (f.flags & 2u) {
-            for (unsigned i = threadIdx.x; i < f.len; i += kFinNT) {
-                data_k[f.start + i] = sk[f.start + i];
-                if constexpr (KV) data_v[f.start + i] = sv[f.start + i];
-            }
-        } else if (f.len <= leaf) {
-            if (threadIdx.x < 32) warp_sort_any2<K, V>(sk + f.start, sv ? sv + f.start : nullptr, data_k + f.start,
-                                                       data_v ? data_v + f.start : nullptr, f.len);
-        } else {
-            fin_local_sort<K, V>(sm, sk, sv, data_k, data_v, f.start, f.len, seed, leaf);
-        }
-    }
-}
-
 // ------------------------------------------------------------ segments API
 // Batched bitonic over CSR segments (config 2): one warp per segment,
 // in place, lengths <= 256 (longer segments flag kErrTooLong, untouched).

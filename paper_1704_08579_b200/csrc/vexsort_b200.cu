@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "partition2.cuh"
 #include "qsort.cuh"
+#include "finish.cuh"
 
 using namespace vx;
 
@@ -87,7 +88,7 @@ struct SortLayout {
         off_spl = o; o = align_up(o + cap_spl * sizeof(K));
         off_bkt = o; o = align_up(o + cap_bkt * sizeof(unsigned long long));
         off_tile = o; o = align_up(o + cap_tiles * sizeof(unsigned));
-        off_fin = o; o = align_up(o + cap_fin * sizeof(Fin));
+        off_fin = o; o = align_up(o + 2 * cap_fin * sizeof(Fin));  // ping-pong by level parity
         total = o;
     }
 };
@@ -190,8 +191,11 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     K* spl = reinterpret_cast<K*>(w + lay.off_spl);
     unsigned long long* bkt = reinterpret_cast<unsigned long long*>(w + lay.off_bkt);
     unsigned* towner = reinterpret_cast<unsigned*>(w + lay.off_tile);
-    Fin* fins = reinterpret_cast<Fin*>(w + lay.off_fin);
+    Fin* fins[2] = {reinterpret_cast<Fin*>(w + lay.off_fin), reinterpret_cast<Fin*>(w + lay.off_fin) + lay.cap_fin};
     if (!HasVal<V>::value) sv = nullptr;
+    // the bitonic leaf bound: the reference's sort_bound when given, else
+    // the widest warp network (512); see DESIGN.md
+    const unsigned leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
 
     const int sms = num_sms();
     static int occ_hist = prepare(qs_hist_kernel<K>, kQsNT, 0);
@@ -202,69 +206,73 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     VX_CUDA(cudaMemsetAsync(ctl, 0, kMaxLevels * sizeof(Ctl), st));
     unsigned long long* hp = g_pinned.get();
     if (!hp) return fail(VX_ECUDA, "cudaHostAlloc failed");
+    unsigned nseg = 0;
+    const K* root_scr_k = sk;
+    const V* root_scr_v = sv;
     if (n <= L::LOCAL) {
         // the whole array is one finish item; its source is the input
         Fin f{0ull, (unsigned)n, in_k == keys ? 0u : 1u};
-        VX_CUDA(cudaMemcpyAsync(fins, &f, sizeof(Fin), cudaMemcpyHostToDevice, st));
+        VX_CUDA(cudaMemcpyAsync(fins[0], &f, sizeof(Fin), cudaMemcpyHostToDevice, st));
         unsigned one = 1;
         VX_CUDA(cudaMemcpyAsync(&ctl[0].fin_ctr, &one, sizeof(unsigned), cudaMemcpyHostToDevice, st));
-        {
-            Launch l(KC_FINISH, st);
-            qs_finish_kernel<K, V><<<1, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, ctl, keys, vals, in_k, in_v, seed,
-                                                                             (unsigned)bound);
-        }
+        root_scr_k = in_k;
+        root_scr_v = in_v;
+    } else {
+        qs_init_kernel<<<1, 1, 0, st>>>(segs[0], ctl, n);
         VX_LAUNCHED();
-        if (g_prof.on) prof_elems(KC_FINISH, n);
-        return VX_OK;
+        nseg = 1;
     }
-    qs_init_kernel<<<1, 1, 0, st>>>(segs[0], ctl, n);
-    VX_LAUNCHED();
-    unsigned nseg = 1;
     for (int level = 0; level < kMaxLevels - 1; ++level) {
         const bool even = (level & 1) == 0;
-        const K* src_k = level == 0 ? in_k : (even ? keys : sk);
-        const V* src_v = level == 0 ? in_v : (even ? vals : sv);
-        K* dst_k = even ? sk : keys;
-        V* dst_v = even ? sv : vals;
         Ctl* c = ctl + level;
         const uint64_t lvl_seed = mix64(seed + 0x51ED270B27AD1CULL * (level + 1));
-        const unsigned g_seg = std::min<unsigned>(nseg, (unsigned)sms * 4);
-        {
-            Launch l(KC_PLAN, st);
-            qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, segs[level & 1], c, spl, bkt, towner,
-                                                             (unsigned)lay.cap_spl, (unsigned)lay.cap_bkt,
-                                                             (unsigned)lay.cap_tiles, lvl_seed);
+        if (nseg > 0) {
+            const K* src_k = level == 0 ? in_k : (even ? keys : sk);
+            const V* src_v = level == 0 ? in_v : (even ? vals : sv);
+            K* dst_k = even ? sk : keys;
+            V* dst_v = even ? sv : vals;
+            const unsigned g_seg = std::min<unsigned>(nseg, (unsigned)sms * 4);
+            {
+                Launch l(KC_PLAN, st);
+                qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, segs[level & 1], c, spl, bkt, towner,
+                                                                 (unsigned)lay.cap_spl, (unsigned)lay.cap_bkt,
+                                                                 (unsigned)lay.cap_tiles, lvl_seed);
+            }
+            VX_LAUNCHED();
+            {
+                Launch l(KC_HIST, st);
+                qs_hist_kernel<K><<<g_hist, kQsNT, 0, st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
+            }
+            VX_LAUNCHED();
+            {
+                Launch l(KC_EMIT, st);
+                qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
+                                                                 segs[(level + 1) & 1], bkt, fins[level & 1],
+                                                                 (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
+                                                                 even ? 1 : 0);
+            }
+            VX_LAUNCHED();
+            {
+                Launch l(KC_SCATTER, st);
+                qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterSmem<K, V>), st>>>(
+                    src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
+            }
+            VX_LAUNCHED();
         }
-        VX_LAUNCHED();
-        {
-            Launch l(KC_HIST, st);
-            qs_hist_kernel<K><<<g_hist, kQsNT, 0, st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
-        }
-        VX_LAUNCHED();
-        {
-            Launch l(KC_EMIT, st);
-            qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
-                                                             segs[(level + 1) & 1], bkt, fins,
-                                                             (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
-                                                             even ? 1 : 0);
-        }
-        VX_LAUNCHED();
-        {
-            Launch l(KC_SCATTER, st);
-            qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterSmem<K, V>), st>>>(
-                src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
-        }
-        VX_LAUNCHED();
         {
             Launch l(KC_FINISH, st);
-            qs_finish_kernel<K, V><<<g_fin, kFinNT, sizeof(FinSmem<K, V>), st>>>(fins, c, keys, vals, sk, sv,
-                                                                                lvl_seed, (unsigned)bound);
+            const K* scr_k = level == 0 ? root_scr_k : sk;
+            const V* scr_v = level == 0 ? root_scr_v : sv;
+            qs_finish_kernel<K, V><<<g_fin, kFinNT, sizeof(FinSmem<K, V>), st>>>(
+                fins[level & 1], c, ctl + level + 1, fins[(level + 1) & 1], (unsigned)lay.cap_fin, keys, vals, scr_k,
+                scr_v, lvl_seed, leaf);
         }
         VX_LAUNCHED();
-        // next level's queue size, error flags and element counters -> host
+        // next level's queue sizes, error flags and element counters -> host
         VX_CUDA(cudaMemcpyAsync(hp, &ctl[level + 1].nseg, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaMemcpyAsync(hp + 1, &c->err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaMemcpyAsync(hp + 2, &c->scat_elems, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        VX_CUDA(cudaMemcpyAsync(hp + 4, &ctl[level + 1].fin_ctr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaStreamSynchronize(st));
         if (g_prof.on) {
             prof_elems(KC_SCATTER, hp[2]);
@@ -273,7 +281,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         }
         if ((unsigned)hp[1]) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
         nseg = (unsigned)hp[0];
-        if (nseg == 0) return VX_OK;
+        if (nseg == 0 && (unsigned)hp[4] == 0) return VX_OK;
     }
     return fail(VX_ECAPACITY, "sort exceeded the maximum level count");
 }
