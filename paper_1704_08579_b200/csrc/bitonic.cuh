@@ -54,19 +54,40 @@ struct WarpBitonic {
             constexpr int HB = 1 << (31 - __builtin_clz(LM));  // highest lane bit
             const int lane = threadIdx.x & 31;
             const bool low = (lane & HB) == 0;
-            K pk[E];
-            V pv[E];
+            // low side takes the partner iff partner < mine; high side iff
+            // mine < partner.  Registers r and r^RM are exchanged as a pair so
+            // both shuffles read the old values without a full copy.
+            if constexpr (RM == 0) {
 #pragma unroll
-            for (int r = 0; r < E; ++r) {
-                pk[r] = __shfl_xor_sync(0xffffffffu, k[r ^ RM], LM);
-                if constexpr (KV) pv[r] = __shfl_xor_sync(0xffffffffu, v[r ^ RM], LM);
+                for (int r = 0; r < E; ++r) {
+                    const K p = __shfl_xor_sync(0xffffffffu, k[r], LM);
+                    V q;
+                    if constexpr (KV) q = __shfl_xor_sync(0xffffffffu, v[r], LM);
+                    const bool t = low ? (p < k[r]) : (k[r] < p);
+                    k[r] = t ? p : k[r];
+                    if constexpr (KV) v[r] = t ? q : v[r];
+                }
+                return;
             }
 #pragma unroll
             for (int r = 0; r < E; ++r) {
-                // low side takes the partner iff partner < mine; high side iff mine < partner
-                bool take = low ? (pk[r] < k[r]) : (k[r] < pk[r]);
-                k[r] = take ? pk[r] : k[r];
-                if constexpr (KV) v[r] = take ? pv[r] : v[r];
+                const int r2 = r ^ RM;
+                if (r2 < r) continue;
+                const K p1 = __shfl_xor_sync(0xffffffffu, k[r2], LM);
+                const K p2 = __shfl_xor_sync(0xffffffffu, k[r], LM);
+                V q1, q2;
+                if constexpr (KV) {
+                    q1 = __shfl_xor_sync(0xffffffffu, v[r2], LM);
+                    q2 = __shfl_xor_sync(0xffffffffu, v[r], LM);
+                }
+                const bool t1 = low ? (p1 < k[r]) : (k[r] < p1);
+                const bool t2 = low ? (p2 < k[r2]) : (k[r2] < p2);
+                k[r] = t1 ? p1 : k[r];
+                if constexpr (KV) v[r] = t1 ? q1 : v[r];
+                if (r2 != r) {
+                    k[r2] = t2 ? p2 : k[r2];
+                    if constexpr (KV) v[r2] = t2 ? q2 : v[r2];
+                }
             }
         }
     }

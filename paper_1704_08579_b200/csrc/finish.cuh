@@ -29,7 +29,7 @@ namespace vx {
 constexpr int kFinMaxSplit = 63;
 constexpr int kFinMaxBkt = 2 * kFinMaxSplit + 1;
 constexpr int kFinMaxSample = 512;
-constexpr unsigned kWarpSortMax = 512;
+constexpr unsigned kWarpSortMax = 256;
 
 __device__ __forceinline__ unsigned pad32(unsigned i) { return i + (i >> 5); }
 
@@ -41,6 +41,7 @@ struct FinSmem {
     K b[PCAP];
     VS bv[HasVal<V>::value ? PCAP : 1];
     K samp[kFinMaxSample];
+    K samp2[kFinMaxSample];
     K spl[kFinMaxSplit + 1];
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
@@ -78,8 +79,8 @@ __device__ __forceinline__ void warp_sort_smem(K* b, V* bv, unsigned lo, unsigne
     if (c <= 32) warp_sort_smem_e<K, V, 1>(b, bv, lo, c);
     else if (c <= 64) warp_sort_smem_e<K, V, 2>(b, bv, lo, c);
     else if (c <= 128) warp_sort_smem_e<K, V, 4>(b, bv, lo, c);
-    else if (c <= 256) warp_sort_smem_e<K, V, 8>(b, bv, lo, c);
-    else warp_sort_smem_e<K, V, 16>(b, bv, lo, c);
+    else warp_sort_smem_e<K, V, 8>(b, bv, lo, c);
+    // callers never pass c > kWarpSortMax (256)
 }
 
 // sort the S (pow2, 32..512) samples of smem `s` ascending with one warp
@@ -101,9 +102,7 @@ __device__ __forceinline__ void warp_sort_samples(K* s, unsigned S) {
     switch (S) {
         case 32: run(std::integral_constant<int, 1>{}); break;
         case 64: run(std::integral_constant<int, 2>{}); break;
-        case 128: run(std::integral_constant<int, 4>{}); break;
-        case 256: run(std::integral_constant<int, 8>{}); break;
-        default: run(std::integral_constant<int, 16>{}); break;
+        default: run(std::integral_constant<int, 4>{}); break;  // 128-sample chunks
     }
     __syncwarp();
 }
@@ -118,7 +117,60 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     constexpr int NW = kFinNT / 32;
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // 1. the range into registers, striped and coalesced
+    // 1. stratified sample read straight from global, sorted by warp 0
+    const unsigned target = max(2u, min(112u, leaf * 7 / 16));
+    const unsigned mt = max(1u, min((unsigned)kFinMaxSplit, len / target));
+    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(8 * (mt + 1))));
+    if (tid < S) {
+        const unsigned stride = max(1u, len / S);
+        const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
+        const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
+        sm.samp[tid] = src_k[start + q];
+    }
+    __syncthreads();
+    // up to 4 warps sort 128-sample chunks in registers, then the chunks are
+    // merged by rank (position = own index + ranks in the other chunks)
+    const unsigned C = min(S, 128u), W = S / C;
+    if (warp < W) warp_sort_samples<K>(sm.samp + warp * C, C);
+    __syncthreads();
+    if (W > 1) {
+        if (tid < S) {
+            const K v = sm.samp[tid];
+            const unsigned c = tid / C;
+            unsigned pos = tid % C;
+            for (unsigned o = 0; o < W; ++o) {
+                if (o == c) continue;
+                const K* ch = sm.samp + o * C;
+                unsigned lo = 0, hi = C;  // o < c: count(<= v); o > c: count(< v)
+                while (lo < hi) {
+                    const unsigned mid = (lo + hi) >> 1;
+                    const bool before = o < c ? !(v < ch[mid]) : (ch[mid] < v);
+                    if (before) lo = mid + 1; else hi = mid;
+                }
+                pos += lo;
+            }
+            sm.samp2[pos] = v;
+        }
+        __syncthreads();
+    }
+    const K* samp = W > 1 ? sm.samp2 : sm.samp;
+    // 3. distinct pivots
+    K cand = K();
+    unsigned keep = 0;
+    if (tid < mt) {
+        const unsigned q = (unsigned)(((uint64_t)(tid + 1) * S) / (mt + 1));
+        cand = samp[q];
+        keep = tid == 0 ? 1u : (samp[(unsigned)(((uint64_t)tid * S) / (mt + 1))] < cand ? 1u : 0u);
+    }
+    unsigned m;
+    const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
+    const unsigned span = next_pow2_u32(m + 1);
+    const unsigned nb = 2 * m + 1;
+    if (keep) sm.spl[rank] = cand;
+    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<K>::sentinel();
+    if (tid < nb) sm.cnt[tid] = 0;
+    // 2. the range into registers, striped and coalesced (only now, so the
+    //    sample network above does not hold them live)
     K x[IPT];
     V y[IPT];
 #pragma unroll
@@ -129,34 +181,6 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
             if constexpr (KV) y[j] = ld_stream(src_v + start + p);
         }
     }
-    // 2. stratified sample (L1/L2-resident re-read), sorted by warp 0
-    const unsigned target = max(2u, min(128u, leaf / 2));
-    const unsigned mt = max(1u, min((unsigned)kFinMaxSplit, len / target));
-    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(8 * (mt + 1))));
-    if (tid < S) {
-        const unsigned stride = max(1u, len / S);
-        const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
-        const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
-        sm.samp[tid] = src_k[start + q];
-    }
-    __syncthreads();
-    if (warp == 0) warp_sort_samples<K>(sm.samp, S);
-    __syncthreads();
-    // 3. distinct pivots
-    K cand = K();
-    unsigned keep = 0;
-    if (tid < mt) {
-        const unsigned q = (unsigned)(((uint64_t)(tid + 1) * S) / (mt + 1));
-        cand = sm.samp[q];
-        keep = tid == 0 ? 1u : (sm.samp[(unsigned)(((uint64_t)tid * S) / (mt + 1))] < cand ? 1u : 0u);
-    }
-    unsigned m;
-    const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
-    const unsigned span = next_pow2_u32(m + 1);
-    const unsigned nb = 2 * m + 1;
-    if (keep) sm.spl[rank] = cand;
-    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<K>::sentinel();
-    if (tid < nb) sm.cnt[tid] = 0;
     __syncthreads();
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
     unsigned br[IPT];
@@ -221,7 +245,7 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
 // warp bitonic (len <= leaf), or the CTA-local sort above.  Source is the
 // scratch buffer when flags bit0 is set, else `data` (in place).
 template <typename K, typename V>
-__global__ void __launch_bounds__(kFinNT) qs_finish_kernel(const Fin* __restrict__ fins, Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(kFinNT, 2) qs_finish_kernel(const Fin* __restrict__ fins, Ctl* __restrict__ ctl,
                                                            Ctl* __restrict__ ctl_next, Fin* __restrict__ fins_next,
                                                            unsigned cap_fin, K* __restrict__ data_k,
                                                            V* __restrict__ data_v, const K* __restrict__ scr_k,
