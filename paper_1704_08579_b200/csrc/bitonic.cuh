@@ -15,78 +15,74 @@
 // register r of `lane` (blocked).  Comparators whose XOR distance is < E are
 // in-register; larger distances cross lanes with __shfl_xor_sync (lane mask
 // = dist / E, register mask = dist % E).  Each side of a cross-lane pair
-// computes its own half from the *old* values, so all partner values are
-// gathered before any update.
+// computes its own half from the *old* values.
+//
+// Everything is branch-free: keys-only comparators are min/max (one
+// VIMNMX / DMNMX each, the lane's side picked by a per-round predicate);
+// key/value comparators use a strict-inversion predicate and selects.
 #pragma once
 
 #include "common.cuh"
 
 namespace vx {
 
+__device__ __forceinline__ int32_t kmin(int32_t a, int32_t b) { return min(a, b); }
+__device__ __forceinline__ int32_t kmax(int32_t a, int32_t b) { return max(a, b); }
+__device__ __forceinline__ double kmin(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ double kmax(double a, double b) { return fmax(a, b); }
+
 template <typename K, typename V, int E>
 struct WarpBitonic {
     static constexpr int P = 32 * E;
     static constexpr bool KV = HasVal<V>::value;
 
-    // one comparator round with XOR distance `mask` over all P slots
+    // one comparator round with XOR distance MASK over all P slots
     template <int MASK>
     __device__ __forceinline__ static void round(K (&k)[E], V (&v)[E]) {
         if constexpr (MASK < E) {
 #pragma unroll
             for (int r = 0; r < E; ++r) {
                 const int r2 = r ^ MASK;
-                if (r < r2) {
-                    // slot r is the lower index: minimum stays at r
-                    K a = k[r], b = k[r2];
-                    bool sw = b < a;  // strict inversion; equals (a<=b ? a : b) for keys
-                    k[r] = sw ? b : a;
-                    k[r2] = sw ? a : b;
+                if (r < r2) {  // slot r is the lower index: minimum stays at r
+                    const K a = k[r], b = k[r2];
                     if constexpr (KV) {
-                        V x = v[r], y = v[r2];
+                        const bool sw = b < a;  // strict inversion only
+                        k[r] = sw ? b : a;
+                        k[r2] = sw ? a : b;
+                        const V x = v[r], y = v[r2];
                         v[r] = sw ? y : x;
                         v[r2] = sw ? x : y;
+                    } else {
+                        k[r] = kmin(a, b);
+                        k[r2] = kmax(a, b);
                     }
                 }
             }
         } else {
-            constexpr int LM = MASK / E;   // lane xor mask
-            constexpr int RM = MASK % E;   // register xor mask (E-1 on crossing rounds, else 0)
+            constexpr int LM = MASK / E;  // lane xor mask
+            constexpr int RM = MASK % E;  // register xor mask (E-1 on crossing rounds, else 0)
             constexpr int HB = 1 << (31 - __builtin_clz(LM));  // highest lane bit
             const int lane = threadIdx.x & 31;
-            const bool low = (lane & HB) == 0;
-            // low side takes the partner iff partner < mine; high side iff
-            // mine < partner.  Registers r and r^RM are exchanged as a pair so
-            // both shuffles read the old values without a full copy.
-            if constexpr (RM == 0) {
+            const bool low = (lane & HB) == 0;  // this lane holds the lower slots
+            // gather every partner value first (old values), then update
+            K pk[E];
+            V pv[E];
 #pragma unroll
-                for (int r = 0; r < E; ++r) {
-                    const K p = __shfl_xor_sync(0xffffffffu, k[r], LM);
-                    V q;
-                    if constexpr (KV) q = __shfl_xor_sync(0xffffffffu, v[r], LM);
-                    const bool t = low ? (p < k[r]) : (k[r] < p);
-                    k[r] = t ? p : k[r];
-                    if constexpr (KV) v[r] = t ? q : v[r];
-                }
-                return;
+            for (int r = 0; r < E; ++r) {
+                pk[r] = __shfl_xor_sync(0xffffffffu, k[r ^ RM], LM);
+                if constexpr (KV) pv[r] = __shfl_xor_sync(0xffffffffu, v[r ^ RM], LM);
             }
 #pragma unroll
             for (int r = 0; r < E; ++r) {
-                const int r2 = r ^ RM;
-                if (r2 < r) continue;
-                const K p1 = __shfl_xor_sync(0xffffffffu, k[r2], LM);
-                const K p2 = __shfl_xor_sync(0xffffffffu, k[r], LM);
-                V q1, q2;
                 if constexpr (KV) {
-                    q1 = __shfl_xor_sync(0xffffffffu, v[r2], LM);
-                    q2 = __shfl_xor_sync(0xffffffffu, v[r], LM);
-                }
-                const bool t1 = low ? (p1 < k[r]) : (k[r] < p1);
-                const bool t2 = low ? (p2 < k[r2]) : (k[r2] < p2);
-                k[r] = t1 ? p1 : k[r];
-                if constexpr (KV) v[r] = t1 ? q1 : v[r];
-                if (r2 != r) {
-                    k[r2] = t2 ? p2 : k[r2];
-                    if constexpr (KV) v[r2] = t2 ? q2 : v[r2];
+                    // low side takes the partner iff partner < mine, high side
+                    // iff partner > mine: strict inversion, branch-free
+                    const int lt = pk[r] < k[r], ne = pk[r] != k[r];
+                    const int t = ne & (lt ^ (int)!low);
+                    k[r] = t ? pk[r] : k[r];
+                    v[r] = t ? pv[r] : v[r];
+                } else {
+                    k[r] = low ? kmin(k[r], pk[r]) : kmax(k[r], pk[r]);
                 }
             }
         }
