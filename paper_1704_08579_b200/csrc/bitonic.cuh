@@ -30,6 +30,8 @@ __device__ __forceinline__ int32_t kmin(int32_t a, int32_t b) { return min(a, b)
 __device__ __forceinline__ int32_t kmax(int32_t a, int32_t b) { return max(a, b); }
 __device__ __forceinline__ double kmin(double a, double b) { return fmin(a, b); }
 __device__ __forceinline__ double kmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ uint64_t kmin(uint64_t a, uint64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ uint64_t kmax(uint64_t a, uint64_t b) { return a < b ? b : a; }
 
 template <typename K, typename V, int E>
 struct WarpBitonic {
@@ -116,22 +118,24 @@ template <typename K, typename V, int E>
 __device__ __forceinline__ void warp_sort_region(const K* src_k, const V* src_v, K* dst_k, V* dst_v,
                                                  uint64_t start, uint32_t len) {
     constexpr bool KV = HasVal<V>::value;
+    using R = KeyRep<K>;
+    using I = typename R::I;
     const int lane = threadIdx.x & 31;
-    K k[E];
+    I k[E];
     V v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const uint32_t q = lane * E + r;
-        k[r] = q < len ? src_k[start + q] : KeyTraits<K>::sentinel();
+        k[r] = q < len ? R::to(src_k[start + q]) : KeyTraits<I>::sentinel();
         if constexpr (KV) v[r] = q < len ? src_v[start + q] : V();
     }
     __syncwarp();
-    WarpBitonic<K, V, E>::sort(k, v);
+    WarpBitonic<I, V, E>::sort(k, v);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const uint32_t q = lane * E + r;
         if (q < len) {
-            dst_k[start + q] = k[r];
+            dst_k[start + q] = R::from(k[r]);
             if constexpr (KV) dst_v[start + q] = v[r];
         }
     }

@@ -24,6 +24,35 @@ struct KeyTraits<double> {
     __host__ __device__ static constexpr double sentinel() { return __builtin_huge_val(); }
 };
 
+// Compare representation.  float64 keys are compared as order-preserving
+// uint64 codes inside the networks and classifiers (integer min/max instead
+// of the FP64 pipe; value order is preserved for every non-NaN key, the one
+// refinement being -0.0 < +0.0, which the reference treats as equal so any
+// order of the two is a correct sort).  int32 keys compare natively.
+template <typename K>
+struct KeyRep {
+    using I = K;
+    __device__ __forceinline__ static I to(K k) { return k; }
+    __device__ __forceinline__ static K from(I i) { return i; }
+};
+template <>
+struct KeyRep<double> {
+    using I = uint64_t;
+    __device__ __forceinline__ static I to(double d) {
+        const uint64_t u = (uint64_t)__double_as_longlong(d);
+        return u ^ ((uint64_t)((int64_t)u >> 63) | 0x8000000000000000ULL);
+    }
+    __device__ __forceinline__ static double from(I o) {
+        const uint64_t m = (o >> 63) ? 0x8000000000000000ULL : ~0ULL;
+        return __longlong_as_double((long long)(o ^ m));
+    }
+};
+template <>
+struct KeyTraits<uint64_t> {
+    // rep of +inf: the largest non-NaN code
+    __host__ __device__ static constexpr uint64_t sentinel() { return 0xFFF0000000000000ULL; }
+};
+
 // "no payload" marker type for key-only instantiations
 struct NoVal {};
 template <typename V>

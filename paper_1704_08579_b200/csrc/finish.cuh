@@ -40,9 +40,10 @@ struct FinSmem {
     using VS = typename std::conditional<HasVal<V>::value, V, char>::type;
     K b[PCAP];
     VS bv[HasVal<V>::value ? PCAP : 1];
-    K samp[kFinMaxSample];
-    K samp2[kFinMaxSample];
-    K spl[kFinMaxSplit + 1];
+    using I = typename KeyRep<K>::I;  // samples and pivots in compare representation
+    I samp[kFinMaxSample];
+    I samp2[kFinMaxSample];
+    I spl[kFinMaxSplit + 1];
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
     unsigned scan[kFinNT / 32 + 1];
@@ -53,21 +54,23 @@ struct FinSmem {
 template <typename K, typename V, int E>
 __device__ __forceinline__ void warp_sort_smem_e(K* b, V* bv, unsigned lo, unsigned c) {
     constexpr bool KV = HasVal<V>::value;
+    using R = KeyRep<K>;
+    using I = typename R::I;
     const unsigned lane = threadIdx.x & 31;
-    K k[E];
+    I k[E];
     V v[E];
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const unsigned q = lane * E + r;
-        k[r] = q < c ? b[pad32(lo + q)] : KeyTraits<K>::sentinel();
+        k[r] = q < c ? R::to(b[pad32(lo + q)]) : KeyTraits<I>::sentinel();
         if constexpr (KV) v[r] = q < c ? bv[pad32(lo + q)] : V();
     }
-    WarpBitonic<K, V, E>::sort(k, v);
+    WarpBitonic<I, V, E>::sort(k, v);
 #pragma unroll
     for (int r = 0; r < E; ++r) {
         const unsigned q = lane * E + r;
         if (q < c) {
-            b[pad32(lo + q)] = k[r];
+            b[pad32(lo + q)] = R::from(k[r]);
             if constexpr (KV) bv[pad32(lo + q)] = v[r];
         }
     }
@@ -115,6 +118,8 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     constexpr unsigned CAP = FinSmem<K, V>::CAP;
     constexpr int IPT = CAP / kFinNT;
     constexpr int NW = kFinNT / 32;
+    using R = KeyRep<K>;
+    using I = typename R::I;
     const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // 1. stratified sample read straight from global, sorted by warp 0
@@ -125,22 +130,22 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         const unsigned stride = max(1u, len / S);
         const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
         const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
-        sm.samp[tid] = src_k[start + q];
+        sm.samp[tid] = R::to(src_k[start + q]);
     }
     __syncthreads();
     // up to 4 warps sort 128-sample chunks in registers, then the chunks are
     // merged by rank (position = own index + ranks in the other chunks)
     const unsigned C = min(S, 128u), W = S / C;
-    if (warp < W) warp_sort_samples<K>(sm.samp + warp * C, C);
+    if (warp < W) warp_sort_samples<I>(sm.samp + warp * C, C);
     __syncthreads();
     if (W > 1) {
         if (tid < S) {
-            const K v = sm.samp[tid];
+            const I v = sm.samp[tid];
             const unsigned c = tid / C;
             unsigned pos = tid % C;
             for (unsigned o = 0; o < W; ++o) {
                 if (o == c) continue;
-                const K* ch = sm.samp + o * C;
+                const I* ch = sm.samp + o * C;
                 unsigned lo = 0, hi = C;  // o < c: count(<= v); o > c: count(< v)
                 while (lo < hi) {
                     const unsigned mid = (lo + hi) >> 1;
@@ -153,9 +158,9 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         }
         __syncthreads();
     }
-    const K* samp = W > 1 ? sm.samp2 : sm.samp;
+    const I* samp = W > 1 ? sm.samp2 : sm.samp;
     // 3. distinct pivots
-    K cand = K();
+    I cand = I();
     unsigned keep = 0;
     if (tid < mt) {
         const unsigned q = (unsigned)(((uint64_t)(tid + 1) * S) / (mt + 1));
@@ -164,10 +169,10 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     }
     unsigned m;
     const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
-    const unsigned span = next_pow2_u32(m + 1);
+    constexpr unsigned span = kFinMaxSplit + 1;  // pivots padded to 64 (fixed-depth search)
     const unsigned nb = 2 * m + 1;
     if (keep) sm.spl[rank] = cand;
-    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<K>::sentinel();
+    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<I>::sentinel();
     if (tid < nb) sm.cnt[tid] = 0;
     // 2. the range into registers, striped and coalesced (only now, so the
     //    sample network above does not hold them live)
@@ -188,7 +193,7 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
         if (p < len) {
-            const unsigned b = cls_eq(x[j], sm.spl, m, span);
+            const unsigned b = cls_eq_u<6>(R::to(x[j]), sm.spl, m);
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
     }

@@ -38,7 +38,7 @@ namespace vx {
 
 constexpr int kMaxSplit = 255;                 // pivots per segment (level)
 constexpr int kMaxBkt = 2 * kMaxSplit + 1;     // 511 buckets
-constexpr int kQsNT = 256;                     // tile-kernel threads
+constexpr int kQsNT = 512;                     // tile-kernel threads
 constexpr int kPlanNT = 512;                   // plan / emit threads
 constexpr int kFinNT = 512;                    // finish-kernel threads
 constexpr int kMaxSample = 4096;
@@ -47,7 +47,7 @@ constexpr uint32_t kCopyChunk = 16384;
 constexpr int kMaxLevels = 48;
 
 template <typename K>
-struct QsTile { static constexpr int IPT = 16; };   // 4096 int32 / 4096 f64 per tile
+struct QsTile { static constexpr int IPT = 8; };    // 4096 elements per tile
 template <typename K>
 constexpr int qs_tile() { return kQsNT * QsTile<K>::IPT; }
 
@@ -88,6 +88,20 @@ __device__ __forceinline__ unsigned cls_eq(K x, const K* spl, unsigned m, unsign
     // pos is now #{spl[i] < x} restricted to span; equality check
     const unsigned eq = (pos < m) && !(x < spl[pos]);
     return 2 * pos + eq;
+}
+
+// Same classifier over a table padded (with the sentinel) to 2^LOG entries:
+// a fixed, fully unrolled search, so a thread's independent elements
+// interleave their shared-memory loads instead of serialising on latency.
+template <int LOG, typename K>
+__device__ __forceinline__ unsigned cls_eq_u(K x, const K* spl, unsigned m) {
+    unsigned pos = 0;
+#pragma unroll
+    for (int h = LOG - 1; h >= 0; --h) {
+        const unsigned half = 1u << h;
+        pos += (spl[pos + half - 1] < x) ? half : 0u;
+    }
+    return 2 * pos + (unsigned)((pos < m) & (spl[pos] == x));
 }
 
 // (key, global index) classifier for the sharded sort: bucket = number of
@@ -207,20 +221,23 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
 // Load one segment's splitters into smem, padded with the sentinel to a pow2
 // span.  Returns the span.
 template <typename K, int NT>
-__device__ __forceinline__ unsigned load_splitters(K* s_spl, const K* spl_pool, unsigned off, unsigned m) {
-    const unsigned span = next_pow2_u32(m + 1);
-    for (unsigned i = threadIdx.x; i < span; i += NT) s_spl[i] = i < m ? spl_pool[off + i] : KeyTraits<K>::sentinel();
-    return span;
+__device__ __forceinline__ unsigned load_splitters(typename KeyRep<K>::I* s_spl, const K* spl_pool, unsigned off,
+                                                   unsigned m) {
+    using I = typename KeyRep<K>::I;
+    // always padded to 256 entries for the fixed-depth classifier
+    for (unsigned i = threadIdx.x; i < 256; i += NT)
+        s_spl[i] = i < m ? KeyRep<K>::to(spl_pool[off + i]) : KeyTraits<I>::sentinel();
+    return 256;
 }
 
 // ------------------------------------------------------------ hist
 template <typename K>
-__global__ void __launch_bounds__(kQsNT) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
+__global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
                                                         const Ctl* __restrict__ ctl, const unsigned* __restrict__ tile_owner,
                                                         const K* __restrict__ spl_pool,
                                                         unsigned long long* __restrict__ bkt_pool) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    __shared__ K s_spl[256];
+    __shared__ typename KeyRep<K>::I s_spl[256];
     __shared__ unsigned s_hist[kMaxBkt + 1];
     const unsigned ntiles = ctl->tile_ctr;
     unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
@@ -243,14 +260,20 @@ __global__ void __launch_bounds__(kQsNT) qs_hist_kernel(const K* __restrict__ sr
         __syncthreads();
         const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
         const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
+        // all loads first, then the unrolled classifiers (ILP across items)
+        typename KeyRep<K>::I xs[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
-            if (idx < tn) {
-                const K x = ld_stream(src + base + idx);
-                atomicAdd(&s_hist[cls_eq(x, s_spl, m, span)], 1u);
-            }
+            xs[i] = KeyRep<K>::to(idx < tn ? ld_stream(src + base + idx) : K());
         }
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + threadIdx.x;
+            const unsigned b = cls_eq_u<8>(xs[i], s_spl, m);
+            if (idx < tn) atomicAdd(&s_hist[b], 1u);
+        }
+        (void)span;
         __syncthreads();
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT)
             if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
@@ -356,7 +379,7 @@ struct ScatterSmem {
     unsigned cnt[kMaxBkt + 1];
     unsigned loc[kMaxBkt + 1];
     unsigned long long gbase[kMaxBkt + 1];
-    K spl[256];
+    typename KeyRep<K>::I spl[256];  // splitters in compare representation
     unsigned scan[kQsNT / 32 + 1];
 };
 
@@ -368,10 +391,11 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
                                              const unsigned (&bk)[IPT], unsigned validmask, unsigned nb,
                                              unsigned long long* cursor, K* dst_k, V* dst_v, unsigned tn) {
     constexpr bool KV = HasVal<V>::value;
-    unsigned rank[IPT];
+    // rank inside the tile, packed next to the bucket id: (bucket << 16) | rank
+    unsigned br[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i)
-        if ((validmask >> i) & 1u) rank[i] = atomicAdd(&sm.cnt[bk[i]], 1u);
+        br[i] = ((validmask >> i) & 1u) ? ((bk[i] << 16) | atomicAdd(&sm.cnt[bk[i]], 1u)) : 0u;
     __syncthreads();
     // exclusive scan of counts over nb (<= 2*NT) buckets: 2 per thread
     const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;
@@ -390,10 +414,10 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         if ((validmask >> i) & 1u) {
-            const unsigned slot = sm.loc[bk[i]] + rank[i];
+            const unsigned slot = sm.loc[br[i] >> 16] + (br[i] & 0xffffu);
             sm.k[slot] = k[i];
             if constexpr (KV) sm.v[slot] = v[i];
-            sm.b[slot] = (unsigned short)bk[i];
+            sm.b[slot] = (unsigned short)(br[i] >> 16);
         }
     }
     __syncthreads();
@@ -406,7 +430,7 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v,
                                                            const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
                                                            const unsigned* __restrict__ tile_owner,
@@ -448,10 +472,14 @@ __global__ void __launch_bounds__(kQsNT) qs_scatter_kernel(const K* __restrict__
             if (idx < tn) {
                 k[i] = ld_stream(src_k + base + idx);
                 if constexpr (KV) v[i] = ld_stream(src_v + base + idx);
-                bk[i] = cls_eq(k[i], sm.spl, m, span);
                 valid |= 1u << i;
+            } else {
+                k[i] = K();
             }
         }
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) bk[i] = cls_eq_u<8>(KeyRep<K>::to(k[i]), sm.spl, m);
+        (void)span;
         tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, tn);
     }
 }
@@ -485,11 +513,11 @@ __global__ void __launch_bounds__(kQsNT) bp_hist_kernel(const K* __restrict__ sr
                                                         const K* __restrict__ spk, const uint64_t* __restrict__ spi,
                                                         unsigned m, unsigned long long* __restrict__ counts) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    __shared__ K s_k[256];
+    __shared__ typename KeyRep<K>::I s_k[256];
     __shared__ uint64_t s_i[256];
     __shared__ unsigned s_hist[257];
     for (unsigned i = threadIdx.x; i < m; i += kQsNT) {
-        s_k[i] = spk[i];
+        s_k[i] = KeyRep<K>::to(spk[i]);
         s_i[i] = spi[i];
     }
     const uint64_t ntiles = (n + TILE - 1) / TILE;
@@ -504,7 +532,7 @@ __global__ void __launch_bounds__(kQsNT) bp_hist_kernel(const K* __restrict__ sr
             const unsigned idx = i * kQsNT + threadIdx.x;
             if (idx < tn) {
                 const K x = ld_stream(src + base + idx);
-                atomicAdd(&s_hist[cls_idx(x, gofs + base + idx, s_k, s_i, m)], 1u);
+                atomicAdd(&s_hist[cls_idx(KeyRep<K>::to(x), gofs + base + idx, s_k, s_i, m)], 1u);
             }
         }
         __syncthreads();
@@ -525,7 +553,7 @@ __global__ void bp_scan_kernel(const unsigned long long* __restrict__ counts, un
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQsNT) bp_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+__global__ void __launch_bounds__(kQsNT, 2) bp_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t n,
                                                            uint64_t gofs, const K* __restrict__ spk,
                                                            const uint64_t* __restrict__ spi, unsigned m,
@@ -536,7 +564,7 @@ __global__ void __launch_bounds__(kQsNT) bp_scatter_kernel(const K* __restrict__
     ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
     __shared__ uint64_t s_i[256];
     for (unsigned i = threadIdx.x; i < m; i += kQsNT) {
-        sm.spl[i] = spk[i];
+        sm.spl[i] = KeyRep<K>::to(spk[i]);
         s_i[i] = spi[i];
     }
     const unsigned nb = m + 1;
@@ -557,7 +585,7 @@ __global__ void __launch_bounds__(kQsNT) bp_scatter_kernel(const K* __restrict__
             if (idx < tn) {
                 k[i] = ld_stream(src_k + base + idx);
                 if constexpr (KV) v[i] = ld_stream(src_v + base + idx);
-                bk[i] = cls_idx(k[i], gofs + base + idx, sm.spl, s_i, m);
+                bk[i] = cls_idx(KeyRep<K>::to(k[i]), gofs + base + idx, sm.spl, s_i, m);
                 valid |= 1u << i;
             }
         }
