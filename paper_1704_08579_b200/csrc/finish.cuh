@@ -44,6 +44,7 @@ struct FinSmem {
     I samp[kFinMaxSample];
     I samp2[kFinMaxSample];
     I spl[kFinMaxSplit + 1];
+    I tree[kFinMaxSplit + 1];  // pivots in BFS order for the bank-friendly search
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
     unsigned scan[kFinNT / 32 + 1];
@@ -187,13 +188,15 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         }
     }
     __syncthreads();
+    if (tid >= 1 && tid < span) sm.tree[tid] = eytz_node<6>(sm.spl, tid, m);
+    __syncthreads();
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
     unsigned br[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
         if (p < len) {
-            const unsigned b = cls_eq_u<6>(R::to(x[j]), sm.spl, m);
+            const unsigned b = cls_eytz<6>(R::to(x[j]), sm.tree, sm.spl, m);
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
     }

@@ -104,6 +104,30 @@ __device__ __forceinline__ unsigned cls_eq_u(K x, const K* spl, unsigned m) {
     return 2 * pos + (unsigned)((pos < m) & (spl[pos] == x));
 }
 
+// Same classification with the splitters in BFS (Eytzinger) order: the nodes
+// visited at depth d all lie in tree[2^d, 2^(d+1)), consecutive words, so a
+// warp's lanes hit distinct banks on the first five levels (a plain sorted
+// array sends every probe of the upper levels to the same bank).  `sorted`
+// is the ordinary splitter array, used for the equality test.
+template <int L, typename K>
+__device__ __forceinline__ unsigned cls_eytz(K x, const K* tree, const K* sorted, unsigned m) {
+    unsigned i = 1;
+#pragma unroll
+    for (int d = 0; d < L; ++d) i = 2 * i + (unsigned)(tree[i] < x);
+    const unsigned lb = i - (1u << L);  // #splitters < x
+    return 2 * lb + (unsigned)((lb < m) & (sorted[lb] == x));
+}
+
+// Build the BFS layout of a sorted table padded to 2^L - 1 entries (sentinel
+// beyond m): node k at depth d holds in-order element
+// ((2*(k - 2^d) + 1) << (L-1-d)) - 1.
+template <int L, typename K>
+__device__ __forceinline__ K eytz_node(const K* sorted, unsigned k, unsigned m) {
+    const unsigned d = 31 - __clz(k);
+    const unsigned pos = ((2 * (k - (1u << d)) + 1) << (L - 1 - d)) - 1;
+    return pos < m ? sorted[pos] : KeyTraits<K>::sentinel();
+}
+
 // (key, global index) classifier for the sharded sort: bucket = number of
 // splitters lexicographically below (x, gi); ties between equal keys are
 // broken by global index, which keeps few-unique inputs balanced.
@@ -221,12 +245,14 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
 // Load one segment's splitters into smem, padded with the sentinel to a pow2
 // span.  Returns the span.
 template <typename K, int NT>
-__device__ __forceinline__ unsigned load_splitters(typename KeyRep<K>::I* s_spl, const K* spl_pool, unsigned off,
-                                                   unsigned m) {
+__device__ __forceinline__ unsigned load_splitters(typename KeyRep<K>::I* s_spl, typename KeyRep<K>::I* s_tree,
+                                                   const K* spl_pool, unsigned off, unsigned m) {
     using I = typename KeyRep<K>::I;
-    // always padded to 256 entries for the fixed-depth classifier
+    // sorted table padded to 256 with the sentinel, then its BFS layout
     for (unsigned i = threadIdx.x; i < 256; i += NT)
         s_spl[i] = i < m ? KeyRep<K>::to(spl_pool[off + i]) : KeyTraits<I>::sentinel();
+    __syncthreads();
+    for (unsigned k = threadIdx.x + 1; k < 256; k += NT) s_tree[k] = eytz_node<8>(s_spl, k, m);
     return 256;
 }
 
@@ -238,6 +264,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
                                                         unsigned long long* __restrict__ bkt_pool) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     __shared__ typename KeyRep<K>::I s_spl[256];
+    __shared__ typename KeyRep<K>::I s_tree[256];
     __shared__ unsigned s_hist[kMaxBkt + 1];
     const unsigned ntiles = ctl->tile_ctr;
     unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
@@ -253,7 +280,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
             tile_base = sg.tile_base;
             sstart = sg.start;
             send = sg.start + sg.len;
-            span = load_splitters<K, kQsNT>(s_spl, spl_pool, sg.spl_off, m);
+            span = load_splitters<K, kQsNT>(s_spl, s_tree, spl_pool, sg.spl_off, m);
         }
         const unsigned nb = 2 * m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) s_hist[b] = 0;
@@ -270,7 +297,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
-            const unsigned b = cls_eq_u<8>(xs[i], s_spl, m);
+            const unsigned b = cls_eytz<8>(xs[i], s_tree, s_spl, m);
             if (idx < tn) atomicAdd(&s_hist[b], 1u);
         }
         (void)span;
@@ -379,7 +406,8 @@ struct ScatterSmem {
     unsigned cnt[kMaxBkt + 1];
     unsigned loc[kMaxBkt + 1];
     unsigned long long gbase[kMaxBkt + 1];
-    typename KeyRep<K>::I spl[256];  // splitters in compare representation
+    typename KeyRep<K>::I spl[256];   // splitters in compare representation (sorted)
+    typename KeyRep<K>::I tree[256];  // the same, BFS order
     unsigned scan[kQsNT / 32 + 1];
 };
 
@@ -454,7 +482,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restric
             tile_base = sg.tile_base;
             sstart = sg.start;
             send = sg.start + sg.len;
-            span = load_splitters<K, kQsNT>(sm.spl, spl_pool, sg.spl_off, m);
+            span = load_splitters<K, kQsNT>(sm.spl, sm.tree, spl_pool, sg.spl_off, m);
         }
         const unsigned nb = 2 * m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
@@ -478,7 +506,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restric
             }
         }
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) bk[i] = cls_eq_u<8>(KeyRep<K>::to(k[i]), sm.spl, m);
+        for (int i = 0; i < IPT; ++i) bk[i] = cls_eytz<8>(KeyRep<K>::to(k[i]), sm.tree, sm.spl, m);
         (void)span;
         tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, tn);
     }
