@@ -128,6 +128,93 @@ __device__ __forceinline__ K eytz_node(const K* sorted, unsigned k, unsigned m) 
     return pos < m ? sorted[pos] : KeyTraits<K>::sentinel();
 }
 
+// ---------------------------------------------------- cell-table classifier
+// Keys as order-preserving unsigned codes: int32 -> uint32 (sign bit
+// flipped), float64 -> the uint64 code of KeyRep<double>.
+template <typename K>
+struct OKey;
+template <>
+struct OKey<int32_t> {
+    using U = uint32_t;
+    __device__ __forceinline__ static U of(int32_t k) { return (uint32_t)k ^ 0x80000000u; }
+};
+template <>
+struct OKey<double> {
+    using U = uint64_t;
+    __device__ __forceinline__ static U of(double k) { return KeyRep<double>::to(k); }
+};
+
+constexpr int kLutBits = 12;
+
+// Per-segment classification table: the sorted splitters plus a 4096-cell
+// lookup table over [lo, hi] (the smallest / largest splitter).  Cell c
+// covers codes [lo + c<<shift, lo + (c+1)<<shift); lut[c] packs
+// (#splitters below the cell) | (#splitters inside the cell) << 16, so a key
+// is classified with one table load and, only when splitters share its
+// cell, a search over those few.  Replaces the 8-level tree search (one
+// dependent shared-memory load per level) of the global levels.
+template <typename U>
+struct CellTable {
+    U spl[256];
+    unsigned lut[1 << kLutBits];
+};
+template <typename U>
+struct CellParams {
+    U lo, hi;
+    unsigned shift, m;
+};
+
+template <typename U>
+__device__ __forceinline__ unsigned lower_bound_u(const U* a, unsigned lo, unsigned cnt, U x) {
+    while (cnt > 0) {
+        const unsigned half = cnt >> 1;
+        if (a[lo + half] < x) {
+            lo += half + 1;
+            cnt -= half + 1;
+        } else {
+            cnt = half;
+        }
+    }
+    return lo;
+}
+
+// Load m (>= 1) sorted splitters from the pool and build the table.  All
+// threads of the CTA must call it; contains barriers.
+template <typename K, int NT>
+__device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U>& ct, const K* spl_pool,
+                                                   unsigned off, unsigned m) {
+    using U = typename OKey<K>::U;
+    for (unsigned i = threadIdx.x; i < m; i += NT) ct.spl[i] = OKey<K>::of(spl_pool[off + i]);
+    __syncthreads();
+    CellParams<U> p;
+    p.m = m;
+    p.lo = ct.spl[0];
+    p.hi = ct.spl[m - 1];
+    const U range = p.hi - p.lo;
+    const unsigned bits = range == 0 ? 0u : (unsigned)(8 * sizeof(U)) - (sizeof(U) == 8 ? __clzll((long long)range)
+                                                                                      : __clz((int)range));
+    p.shift = bits > kLutBits ? bits - kLutBits : 0u;
+    const unsigned ncell = (unsigned)(range >> p.shift) + 1;
+    for (unsigned c = threadIdx.x; c < ncell; c += NT) {
+        const U cmin = p.lo + ((U)c << p.shift);
+        const unsigned lbmin = lower_bound_u(ct.spl, 0, m, cmin);
+        const unsigned lbmax = (c + 1 < ncell) ? lower_bound_u(ct.spl, lbmin, m - lbmin, cmin + ((U)1 << p.shift)) : m;
+        ct.lut[c] = lbmin | ((lbmax - lbmin) << 16);
+    }
+    __syncthreads();
+    return p;
+}
+
+// bucket = 2*lb + (x == spl[lb]), lb = #splitters < x (equality buckets odd)
+template <typename U>
+__device__ __forceinline__ unsigned ct_classify(const CellTable<U>& ct, const CellParams<U>& p, U x) {
+    if (x < p.lo) return 0;
+    if (p.hi < x) return 2 * p.m;
+    const unsigned e = ct.lut[(unsigned)((x - p.lo) >> p.shift)];
+    const unsigned lb = lower_bound_u(ct.spl, e & 0xffffu, e >> 16, x);
+    return 2 * lb + (unsigned)(lb < p.m && ct.spl[lb] == x);
+}
+
 // (key, global index) classifier for the sharded sort: bucket = number of
 // splitters lexicographically below (x, gi); ties between equal keys are
 // broken by global index, which keeps few-unique inputs balanced.
@@ -263,44 +350,47 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
                                                         const K* __restrict__ spl_pool,
                                                         unsigned long long* __restrict__ bkt_pool) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    __shared__ typename KeyRep<K>::I s_spl[256];
-    __shared__ typename KeyRep<K>::I s_tree[256];
+    using U = typename OKey<K>::U;
+    __shared__ CellTable<U> s_ct;
     __shared__ unsigned s_hist[kMaxBkt + 1];
     const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0, tile_base = 0;
+    CellParams<U> cp{};
     uint64_t sstart = 0, send = 0;
-    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // contiguous chunk of tiles per CTA: consecutive tiles share a segment,
+    // so its classification table is built once per (CTA, segment)
+    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
+    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    for (unsigned t = t0; t < t1; ++t) {
         const unsigned s = tile_owner[t];
         __syncthreads();
         if (s != cur) {
             cur = s;
             const Seg sg = segs[s];
-            m = sg.m;
             bkt_off = sg.bkt_off;
             tile_base = sg.tile_base;
             sstart = sg.start;
             send = sg.start + sg.len;
-            span = load_splitters<K, kQsNT>(s_spl, s_tree, spl_pool, sg.spl_off, m);
+            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);
         }
-        const unsigned nb = 2 * m + 1;
+        const unsigned nb = 2 * cp.m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) s_hist[b] = 0;
         __syncthreads();
         const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
         const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
-        // all loads first, then the unrolled classifiers (ILP across items)
-        typename KeyRep<K>::I xs[IPT];
+        // all loads first, then the classifiers (ILP across items)
+        U xs[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
-            xs[i] = KeyRep<K>::to(idx < tn ? ld_stream(src + base + idx) : K());
+            xs[i] = OKey<K>::of(idx < tn ? ld_stream(src + base + idx) : K());
         }
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
-            const unsigned b = cls_eytz<8>(xs[i], s_tree, s_spl, m);
+            const unsigned b = ct_classify(s_ct, cp, xs[i]);
             if (idx < tn) atomicAdd(&s_hist[b], 1u);
         }
-        (void)span;
         __syncthreads();
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT)
             if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
@@ -406,8 +496,8 @@ struct ScatterSmem {
     unsigned cnt[kMaxBkt + 1];
     unsigned loc[kMaxBkt + 1];
     unsigned long long gbase[kMaxBkt + 1];
-    typename KeyRep<K>::I spl[256];   // splitters in compare representation (sorted)
-    typename KeyRep<K>::I tree[256];  // the same, BFS order
+    CellTable<typename OKey<K>::U> ct;  // splitters + cell lookup table
+    typename KeyRep<K>::I spl[256];     // (key, index) splitters of the sharded bucket partition
     unsigned scan[kQsNT / 32 + 1];
 };
 
@@ -468,23 +558,26 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restric
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
+    using U = typename OKey<K>::U;
     const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, m = 0, span = 1, bkt_off = 0, tile_base = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0, tile_base = 0;
+    CellParams<U> cp{};
     uint64_t sstart = 0, send = 0;
-    for (unsigned t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
+    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    for (unsigned t = t0; t < t1; ++t) {
         const unsigned s = tile_owner[t];
         __syncthreads();
         if (s != cur) {
             cur = s;
             const Seg sg = segs[s];
-            m = sg.m;
             bkt_off = sg.bkt_off;
             tile_base = sg.tile_base;
             sstart = sg.start;
             send = sg.start + sg.len;
-            span = load_splitters<K, kQsNT>(sm.spl, sm.tree, spl_pool, sg.spl_off, m);
+            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m);
         }
-        const unsigned nb = 2 * m + 1;
+        const unsigned nb = 2 * cp.m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
         __syncthreads();
         const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
@@ -506,8 +599,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restric
             }
         }
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) bk[i] = cls_eytz<8>(KeyRep<K>::to(k[i]), sm.tree, sm.spl, m);
-        (void)span;
+        for (int i = 0; i < IPT; ++i) bk[i] = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
         tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, tn);
     }
 }
