@@ -161,7 +161,7 @@ struct CellTable {
 template <typename U>
 struct CellParams {
     U lo, hi;
-    unsigned shift, m;
+    unsigned shift, m, ncell;
 };
 
 template <typename U>
@@ -195,6 +195,7 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
                                                                                       : __clz((int)range));
     p.shift = bits > kLutBits ? bits - kLutBits : 0u;
     const unsigned ncell = (unsigned)(range >> p.shift) + 1;
+    p.ncell = ncell;
     for (unsigned c = threadIdx.x; c < ncell; c += NT) {
         const U cmin = p.lo + ((U)c << p.shift);
         const unsigned lbmin = lower_bound_u(ct.spl, 0, m, cmin);
@@ -206,12 +207,20 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
 }
 
 // bucket = 2*lb + (x == spl[lb]), lb = #splitters < x (equality buckets odd)
+// Keys below lo / above hi clamp into the first / last cell, whose splitter
+// lists contain lo / hi, so no separate branches are needed.  Fast path (no
+// splitter inside the key's cell): one table load, no search, and no
+// equality test (no splitter can equal the key).
 template <typename U>
 __device__ __forceinline__ unsigned ct_classify(const CellTable<U>& ct, const CellParams<U>& p, U x) {
-    if (x < p.lo) return 0;
-    if (p.hi < x) return 2 * p.m;
-    const unsigned e = ct.lut[(unsigned)((x - p.lo) >> p.shift)];
-    const unsigned lb = lower_bound_u(ct.spl, e & 0xffffu, e >> 16, x);
+    const U d = x > p.lo ? x - p.lo : (U)0;
+    const U c64 = d >> p.shift;
+    const unsigned c = c64 < (U)p.ncell ? (unsigned)c64 : p.ncell - 1;
+    const unsigned e = ct.lut[c];
+    unsigned lb = e & 0xffffu;
+    const unsigned cnt = e >> 16;
+    if (cnt == 0) return 2 * lb;
+    lb = lower_bound_u(ct.spl, lb, cnt, x);
     return 2 * lb + (unsigned)(lb < p.m && ct.spl[lb] == x);
 }
 
