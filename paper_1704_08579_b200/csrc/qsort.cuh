@@ -352,6 +352,34 @@ __device__ __forceinline__ unsigned load_splitters(typename KeyRep<K>::I* s_spl,
     return 256;
 }
 
+// ------------------------------------------------------------ tiles
+struct TileGeo {
+    uint64_t base;  // absolute index of the tile's first element
+    unsigned tn;    // elements in the tile
+    unsigned seg;   // owning segment
+};
+
+template <int TILE>
+__device__ __forceinline__ TileGeo tile_geo(unsigned t, const unsigned* tile_owner, const Seg* segs) {
+    TileGeo g;
+    g.seg = tile_owner[t];
+    const uint64_t start = segs[g.seg].start, len = segs[g.seg].len;
+    const unsigned tb = segs[g.seg].tile_base;
+    g.base = start + (uint64_t)(t - tb) * TILE;
+    g.tn = (unsigned)min((uint64_t)TILE, start + len - g.base);
+    return g;
+}
+
+// striped tile load: item i of thread tid is element i*NT + tid
+template <typename T, int IPT>
+__device__ __forceinline__ void load_tile(T (&x)[IPT], const T* src, const TileGeo& g) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+        const unsigned idx = i * kQsNT + threadIdx.x;
+        x[i] = idx < g.tn ? ld_stream(src + g.base + idx) : T();
+    }
+}
+
 // ------------------------------------------------------------ hist
 template <typename K>
 __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
@@ -363,46 +391,46 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
     __shared__ CellTable<U> s_ct;
     __shared__ unsigned s_hist[kMaxBkt + 1];
     const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, bkt_off = 0, tile_base = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0;
     CellParams<U> cp{};
-    uint64_t sstart = 0, send = 0;
     // contiguous chunk of tiles per CTA: consecutive tiles share a segment,
     // so its classification table is built once per (CTA, segment)
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    if (t0 >= t1) return;
+    // register double buffering: tile t+1 is in flight while t is classified
+    TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
+    K xs[IPT];
+    load_tile<K, IPT>(xs, src, g);
     for (unsigned t = t0; t < t1; ++t) {
-        const unsigned s = tile_owner[t];
+        TileGeo gn{};
+        K ys[IPT];
+        if (t + 1 < t1) {
+            gn = tile_geo<TILE>(t + 1, tile_owner, segs);
+            load_tile<K, IPT>(ys, src, gn);
+        }
         __syncthreads();
-        if (s != cur) {
-            cur = s;
-            const Seg sg = segs[s];
+        if (g.seg != cur) {
+            cur = g.seg;
+            const Seg sg = segs[g.seg];
             bkt_off = sg.bkt_off;
-            tile_base = sg.tile_base;
-            sstart = sg.start;
-            send = sg.start + sg.len;
             cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);
         }
         const unsigned nb = 2 * cp.m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) s_hist[b] = 0;
         __syncthreads();
-        const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
-        const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
-        // all loads first, then the classifiers (ILP across items)
-        U xs[IPT];
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
-            xs[i] = OKey<K>::of(idx < tn ? ld_stream(src + base + idx) : K());
-        }
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const unsigned idx = i * kQsNT + threadIdx.x;
-            const unsigned b = ct_classify(s_ct, cp, xs[i]);
-            if (idx < tn) atomicAdd(&s_hist[b], 1u);
+            const unsigned b = ct_classify(s_ct, cp, OKey<K>::of(xs[i]));
+            if (idx < g.tn) atomicAdd(&s_hist[b], 1u);
         }
         __syncthreads();
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT)
             if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) xs[i] = ys[i];
+        g = gn;
     }
 }
 
@@ -569,47 +597,51 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restric
     ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
     using U = typename OKey<K>::U;
     const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, bkt_off = 0, tile_base = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0;
     CellParams<U> cp{};
-    uint64_t sstart = 0, send = 0;
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    if (t0 >= t1) return;
+    // register double buffering: tile t+1 is in flight while t is scattered
+    TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
+    K k[IPT];
+    V v[IPT];
+    load_tile<K, IPT>(k, src_k, g);
+    if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
     for (unsigned t = t0; t < t1; ++t) {
-        const unsigned s = tile_owner[t];
+        TileGeo gn{};
+        K kn[IPT];
+        V vn[IPT];
+        if (t + 1 < t1) {
+            gn = tile_geo<TILE>(t + 1, tile_owner, segs);
+            load_tile<K, IPT>(kn, src_k, gn);
+            if constexpr (KV) load_tile<V, IPT>(vn, src_v, gn);
+        }
         __syncthreads();
-        if (s != cur) {
-            cur = s;
-            const Seg sg = segs[s];
+        if (g.seg != cur) {
+            cur = g.seg;
+            const Seg sg = segs[g.seg];
             bkt_off = sg.bkt_off;
-            tile_base = sg.tile_base;
-            sstart = sg.start;
-            send = sg.start + sg.len;
             cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m);
         }
         const unsigned nb = 2 * cp.m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
         __syncthreads();
-        const uint64_t base = sstart + (uint64_t)(t - tile_base) * TILE;
-        const unsigned tn = (unsigned)min((uint64_t)TILE, send - base);
-        if (threadIdx.x == 0) atomicAdd(&ctl->scat_elems, (unsigned long long)tn);
-        K k[IPT];
-        V v[IPT];
+        if (threadIdx.x == 0) atomicAdd(&ctl->scat_elems, (unsigned long long)g.tn);
         unsigned bk[IPT];
         unsigned valid = 0;
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
-            const unsigned idx = i * kQsNT + threadIdx.x;
-            if (idx < tn) {
-                k[i] = ld_stream(src_k + base + idx);
-                if constexpr (KV) v[i] = ld_stream(src_v + base + idx);
-                valid |= 1u << i;
-            } else {
-                k[i] = K();
-            }
+            if (i * kQsNT + threadIdx.x < g.tn) valid |= 1u << i;
+            bk[i] = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
         }
+        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, g.tn);
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) bk[i] = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
-        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, tn);
+        for (int i = 0; i < IPT; ++i) {
+            k[i] = kn[i];
+            if constexpr (KV) v[i] = vn[i];
+        }
+        g = gn;
     }
 }
 
