@@ -144,7 +144,7 @@ struct OKey<double> {
     __device__ __forceinline__ static U of(double k) { return KeyRep<double>::to(k); }
 };
 
-constexpr int kLutBits = 12;
+constexpr int kLutBits = 13;  // 8192 cells
 
 // Per-segment classification table: the sorted splitters plus a 4096-cell
 // lookup table over [lo, hi] (the smallest / largest splitter).  Cell c
@@ -156,7 +156,7 @@ constexpr int kLutBits = 12;
 template <typename U>
 struct CellTable {
     U spl[256];
-    unsigned lut[1 << kLutBits];
+    unsigned short lut[1 << kLutBits];
 };
 template <typename U>
 struct CellParams {
@@ -200,7 +200,7 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
         const U cmin = p.lo + ((U)c << p.shift);
         const unsigned lbmin = lower_bound_u(ct.spl, 0, m, cmin);
         const unsigned lbmax = (c + 1 < ncell) ? lower_bound_u(ct.spl, lbmin, m - lbmin, cmin + ((U)1 << p.shift)) : m;
-        ct.lut[c] = lbmin | ((lbmax - lbmin) << 16);
+        ct.lut[c] = (unsigned short)(lbmin | ((lbmax - lbmin) << 8));  // m <= 255: 8 | 8 bits
     }
     __syncthreads();
     return p;
@@ -217,9 +217,13 @@ __device__ __forceinline__ unsigned ct_classify(const CellTable<U>& ct, const Ce
     const U c64 = d >> p.shift;
     const unsigned c = c64 < (U)p.ncell ? (unsigned)c64 : p.ncell - 1;
     const unsigned e = ct.lut[c];
-    unsigned lb = e & 0xffffu;
-    const unsigned cnt = e >> 16;
+    unsigned lb = e & 0xffu;
+    const unsigned cnt = e >> 8;
     if (cnt == 0) return 2 * lb;
+    if (cnt == 1) {  // the common slow case: one splitter shares the cell
+        const U s = ct.spl[lb];
+        return 2 * (lb + (unsigned)(s < x)) + (unsigned)(s == x);
+    }
     lb = lower_bound_u(ct.spl, lb, cnt, x);
     return 2 * lb + (unsigned)(lb < p.m && ct.spl[lb] == x);
 }
@@ -409,29 +413,33 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
             gn = tile_geo<TILE>(t + 1, tile_owner, segs);
             load_tile<K, IPT>(ys, src, gn);
         }
-        __syncthreads();
         if (g.seg != cur) {
+            // the smem histogram accumulates over all of this CTA's tiles of
+            // one segment and is flushed once per (CTA, segment)
+            __syncthreads();
+            if (cur != 0xffffffffu)
+                for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT)
+                    if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
             cur = g.seg;
             const Seg sg = segs[g.seg];
             bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);
+            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);  // syncs inside
+            for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
+            __syncthreads();
         }
-        const unsigned nb = 2 * cp.m + 1;
-        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) s_hist[b] = 0;
-        __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned idx = i * kQsNT + threadIdx.x;
             const unsigned b = ct_classify(s_ct, cp, OKey<K>::of(xs[i]));
             if (idx < g.tn) atomicAdd(&s_hist[b], 1u);
         }
-        __syncthreads();
-        for (unsigned b = threadIdx.x; b < nb; b += kQsNT)
-            if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
 #pragma unroll
         for (int i = 0; i < IPT; ++i) xs[i] = ys[i];
         g = gn;
     }
+    __syncthreads();
+    for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT)
+        if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
 }
 
 // ------------------------------------------------------------ emit
