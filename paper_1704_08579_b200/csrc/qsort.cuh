@@ -55,8 +55,9 @@ constexpr int qs_tile() { return kQsNT * QsTile<K>::IPT; }
 template <typename K, typename V>
 struct FinCap {
     static constexpr uint32_t bytes_per = sizeof(K) + (HasVal<V>::value ? sizeof(V) : 0);
-    // power of two so the rare CTA-bitonic fallback (padded) always fits
-    static constexpr uint32_t value = bytes_per <= 4 ? 8192 : (bytes_per <= 8 ? 4096 : 2048);
+    // a multiple of the finish CTA (512 threads); sized so one partition
+    // level of <= 255 pivots takes ~1M-element ranges below it
+    static constexpr uint32_t value = bytes_per <= 4 ? 8192 : (bytes_per <= 8 ? 6144 : 3072);
 };
 
 struct Seg {
