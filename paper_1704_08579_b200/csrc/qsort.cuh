@@ -593,67 +593,6 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
     }
 }
 
-template <typename K, typename V>
-__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
-                                                           K* __restrict__ dst_k, V* __restrict__ dst_v,
-                                                           const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
-                                                           const unsigned* __restrict__ tile_owner,
-                                                           const K* __restrict__ spl_pool,
-                                                           unsigned long long* __restrict__ bkt_pool) {
-    constexpr bool KV = HasVal<V>::value;
-    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    ScatterSmem<K, V>& sm = *reinterpret_cast<ScatterSmem<K, V>*>(smem_raw);
-    using U = typename OKey<K>::U;
-    const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, bkt_off = 0;
-    CellParams<U> cp{};
-    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
-    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
-    if (t0 >= t1) return;
-    // register double buffering: tile t+1 is in flight while t is scattered
-    TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
-    K k[IPT];
-    V v[IPT];
-    load_tile<K, IPT>(k, src_k, g);
-    if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
-    for (unsigned t = t0; t < t1; ++t) {
-        TileGeo gn{};
-        K kn[IPT];
-        V vn[IPT];
-        if (t + 1 < t1) {
-            gn = tile_geo<TILE>(t + 1, tile_owner, segs);
-            load_tile<K, IPT>(kn, src_k, gn);
-            if constexpr (KV) load_tile<V, IPT>(vn, src_v, gn);
-        }
-        __syncthreads();
-        if (g.seg != cur) {
-            cur = g.seg;
-            const Seg sg = segs[g.seg];
-            bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m);
-        }
-        const unsigned nb = 2 * cp.m + 1;
-        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
-        __syncthreads();
-        if (threadIdx.x == 0) atomicAdd(&ctl->scat_elems, (unsigned long long)g.tn);
-        unsigned bk[IPT];
-        unsigned valid = 0;
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            if (i * kQsNT + threadIdx.x < g.tn) valid |= 1u << i;
-            bk[i] = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
-        }
-        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, bkt_pool + bkt_off, dst_k, dst_v, g.tn);
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            k[i] = kn[i];
-            if constexpr (KV) v[i] = vn[i];
-        }
-        g = gn;
-    }
-}
-
 // ------------------------------------------------------------ segments API
 // Batched bitonic over CSR segments (config 2): one warp per segment,
 // in place, lengths <= 256 (longer segments flag kErrTooLong, untouched).

@@ -1,0 +1,138 @@
+// scatter.cuh -- the partition level's scatter pass, software-pipelined.
+//
+// Per 4096-element tile: classify every element against the segment's
+// pivots (cell-table classifier), rank it inside its bucket with a shared
+// memory atomic, reserve one run per non-empty bucket in the destination
+// with a global atomic, stage the tile bucket-major in shared memory and
+// write the runs with consecutive threads (coalesced).  The reservation is
+// a round trip to L2 (~1 us); to keep it off the critical path the write-out
+// of tile t-1 is done while tile t's reservations are in flight (two staging
+// buffers), and tile t+1's loads are already in registers.
+#pragma once
+
+#include "common.cuh"
+#include "qsort.cuh"
+
+namespace vx {
+
+template <typename K, typename V>
+struct ScatterPipeSmem {
+    static constexpr int TILE = qs_tile<K>();
+    using VS = typename std::conditional<HasVal<V>::value, V, char>::type;
+    struct Stage {
+        K k[TILE];
+        VS v[HasVal<V>::value ? TILE : 1];
+        unsigned short b[TILE];
+        unsigned loc[kMaxBkt + 1];
+        unsigned long long gbase[kMaxBkt + 1];
+        unsigned tn;
+    };
+    Stage st[2];
+    unsigned cnt[kMaxBkt + 1];
+    CellTable<typename OKey<K>::U> ct;
+    unsigned scan[kQsNT / 32 + 1];
+};
+
+template <typename K, typename V>
+__device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K, V>::Stage& s, K* dst_k, V* dst_v) {
+    constexpr bool KV = HasVal<V>::value;
+    for (unsigned j = threadIdx.x; j < s.tn; j += kQsNT) {
+        const unsigned b = s.b[j];
+        const unsigned long long pos = s.gbase[b] + (j - s.loc[b]);
+        dst_k[pos] = s.k[j];
+        if constexpr (KV) dst_v[pos] = s.v[j];
+    }
+}
+
+template <typename K, typename V>
+__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+                                                           K* __restrict__ dst_k, V* __restrict__ dst_v,
+                                                           const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
+                                                           const unsigned* __restrict__ tile_owner,
+                                                           const K* __restrict__ spl_pool,
+                                                           unsigned long long* __restrict__ bkt_pool) {
+    constexpr bool KV = HasVal<V>::value;
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    using U = typename OKey<K>::U;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ScatterPipeSmem<K, V>& sm = *reinterpret_cast<ScatterPipeSmem<K, V>*>(smem_raw);
+    const unsigned ntiles = ctl->tile_ctr;
+    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
+    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    if (t0 >= t1) return;
+    unsigned cur = 0xffffffffu, bkt_off = 0;
+    CellParams<U> cp{};
+    TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
+    K k[IPT];
+    V v[IPT];
+    load_tile<K, IPT>(k, src_k, g);
+    if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
+    unsigned long long moved = 0;
+    for (unsigned t = t0; t < t1; ++t) {
+        const int p = (t - t0) & 1;
+        TileGeo gn{};
+        K kn[IPT];
+        V vn[IPT];
+        if (t + 1 < t1) {
+            gn = tile_geo<TILE>(t + 1, tile_owner, segs);
+            load_tile<K, IPT>(kn, src_k, gn);
+            if constexpr (KV) load_tile<V, IPT>(vn, src_v, gn);
+        }
+        if (g.seg != cur) {
+            __syncthreads();
+            cur = g.seg;
+            const Seg sg = segs[g.seg];
+            bkt_off = sg.bkt_off;
+            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m);  // syncs inside
+        }
+        const unsigned nb = 2 * cp.m + 1;
+        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
+        __syncthreads();
+        moved += g.tn;
+        // classify + rank: (bucket << 16) | rank within the tile
+        unsigned br[IPT];
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
+            br[i] = (i * kQsNT + threadIdx.x < g.tn) ? ((b << 16) | atomicAdd(&sm.cnt[b], 1u)) : 0xffffffffu;
+        }
+        __syncthreads();
+        // bucket offsets in the tile (2 buckets per thread) + run reservations
+        typename ScatterPipeSmem<K, V>::Stage& S = sm.st[p];
+        const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;
+        const unsigned c0 = b0 < nb ? sm.cnt[b0] : 0u, c1 = b1 < nb ? sm.cnt[b1] : 0u;
+        unsigned tot;
+        const unsigned ex = block_excl_scan<kQsNT>(c0 + c1, sm.scan, &tot);
+        unsigned long long r0 = 0, r1 = 0;
+        if (c0) r0 = atomicAdd(&bkt_pool[bkt_off + b0], (unsigned long long)c0);
+        if (c1) r1 = atomicAdd(&bkt_pool[bkt_off + b1], (unsigned long long)c1);
+        if (b0 < nb) S.loc[b0] = ex;
+        if (b1 < nb) S.loc[b1] = ex + c0;
+        if (threadIdx.x == 0) S.tn = g.tn;
+        // overlap: write out the previous tile while the reservations fly
+        if (t > t0) stage_writeout<K, V>(sm.st[p ^ 1], dst_k, dst_v);
+        if (c0) S.gbase[b0] = r0;
+        if (c1) S.gbase[b1] = r1;
+        __syncthreads();  // S.loc complete
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            if (br[i] != 0xffffffffu) {
+                const unsigned slot = S.loc[br[i] >> 16] + (br[i] & 0xffffu);
+                S.k[slot] = k[i];
+                if constexpr (KV) S.v[slot] = v[i];
+                S.b[slot] = (unsigned short)(br[i] >> 16);
+            }
+        }
+        __syncthreads();  // stage complete; previous stage free
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            k[i] = kn[i];
+            if constexpr (KV) v[i] = vn[i];
+        }
+        g = gn;
+    }
+    stage_writeout<K, V>(sm.st[(t1 - 1 - t0) & 1], dst_k, dst_v);
+    if (threadIdx.x == 0) atomicAdd(&ctl->scat_elems, moved);
+}
+
+}  // namespace vx

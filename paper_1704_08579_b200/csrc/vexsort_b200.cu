@@ -15,6 +15,7 @@
 #include "partition2.cuh"
 #include "qsort.cuh"
 #include "finish.cuh"
+#include "scatter.cuh"
 
 using namespace vx;
 
@@ -199,7 +200,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
 
     const int sms = num_sms();
     static int occ_hist = prepare(qs_hist_kernel<K>, kQsNT, 0);
-    static int occ_scat = prepare(qs_scatter_kernel<K, V>, kQsNT, sizeof(ScatterSmem<K, V>));
+    static int occ_scat = prepare(qs_scatter_kernel<K, V>, kQsNT, sizeof(ScatterPipeSmem<K, V>));
     static int occ_fin = prepare(qs_finish_kernel<K, V>, kFinNT, sizeof(FinSmem<K, V>));
     const int g_hist = sms * occ_hist, g_scat = sms * occ_scat, g_fin = sms * occ_fin;
 
@@ -254,7 +255,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             VX_LAUNCHED();
             {
                 Launch l(KC_SCATTER, st);
-                qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterSmem<K, V>), st>>>(
+                qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterPipeSmem<K, V>), st>>>(
                     src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
             }
             VX_LAUNCHED();
