@@ -30,6 +30,8 @@ __device__ __forceinline__ int32_t kmin(int32_t a, int32_t b) { return min(a, b)
 __device__ __forceinline__ int32_t kmax(int32_t a, int32_t b) { return max(a, b); }
 __device__ __forceinline__ double kmin(double a, double b) { return fmin(a, b); }
 __device__ __forceinline__ double kmax(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ uint32_t kmin(uint32_t a, uint32_t b) { return min(a, b); }
+__device__ __forceinline__ uint32_t kmax(uint32_t a, uint32_t b) { return max(a, b); }
 __device__ __forceinline__ uint64_t kmin(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint64_t kmax(uint64_t a, uint64_t b) { return a < b ? b : a; }
 

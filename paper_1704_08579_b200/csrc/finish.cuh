@@ -40,11 +40,11 @@ struct FinSmem {
     using VS = typename std::conditional<HasVal<V>::value, V, char>::type;
     K b[PCAP];
     VS bv[HasVal<V>::value ? PCAP : 1];
-    using I = typename KeyRep<K>::I;  // samples and pivots in compare representation
-    I samp[kFinMaxSample];
-    I samp2[kFinMaxSample];
-    I spl[kFinMaxSplit + 1];
-    I tree[kFinMaxSplit + 1];  // pivots in BFS order for the bank-friendly search
+    using U = typename OKey<K>::U;  // samples and pivots as order-preserving codes
+    U samp[kFinMaxSample];
+    U samp2[kFinMaxSample];
+    CellTableT<U, kFinMaxSplit + 1, 9> ct;  // pivots + 512-cell lookup table
+    unsigned next_bucket;
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
     unsigned scan[kFinNT / 32 + 1];
@@ -118,10 +118,8 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     constexpr bool KV = HasVal<V>::value;
     constexpr unsigned CAP = FinSmem<K, V>::CAP;
     constexpr int IPT = CAP / kFinNT;
-    constexpr int NW = kFinNT / 32;
-    using R = KeyRep<K>;
-    using I = typename R::I;
-    const unsigned tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    using U = typename OKey<K>::U;
+    const unsigned tid = threadIdx.x, lane = tid & 31;
 
     // 1. stratified sample read straight from global, sorted by warp 0
     const unsigned target = max(2u, min(112u, leaf * 7 / 16));
@@ -131,22 +129,22 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         const unsigned stride = max(1u, len / S);
         const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
         const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
-        sm.samp[tid] = R::to(src_k[start + q]);
+        sm.samp[tid] = OKey<K>::of(src_k[start + q]);
     }
     __syncthreads();
     // up to 4 warps sort 128-sample chunks in registers, then the chunks are
     // merged by rank (position = own index + ranks in the other chunks)
     const unsigned C = min(S, 128u), W = S / C;
-    if (warp < W) warp_sort_samples<I>(sm.samp + warp * C, C);
+    if ((tid >> 5) < W) warp_sort_samples<U>(sm.samp + (tid >> 5) * C, C);
     __syncthreads();
     if (W > 1) {
         if (tid < S) {
-            const I v = sm.samp[tid];
+            const U v = sm.samp[tid];
             const unsigned c = tid / C;
             unsigned pos = tid % C;
             for (unsigned o = 0; o < W; ++o) {
                 if (o == c) continue;
-                const I* ch = sm.samp + o * C;
+                const U* ch = sm.samp + o * C;
                 unsigned lo = 0, hi = C;  // o < c: count(<= v); o > c: count(< v)
                 while (lo < hi) {
                     const unsigned mid = (lo + hi) >> 1;
@@ -159,9 +157,9 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         }
         __syncthreads();
     }
-    const I* samp = W > 1 ? sm.samp2 : sm.samp;
+    const U* samp = W > 1 ? sm.samp2 : sm.samp;
     // 3. distinct pivots
-    I cand = I();
+    U cand = U();
     unsigned keep = 0;
     if (tid < mt) {
         const unsigned q = (unsigned)(((uint64_t)(tid + 1) * S) / (mt + 1));
@@ -170,11 +168,10 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     }
     unsigned m;
     const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
-    constexpr unsigned span = kFinMaxSplit + 1;  // pivots padded to 64 (fixed-depth search)
     const unsigned nb = 2 * m + 1;
-    if (keep) sm.spl[rank] = cand;
-    if (tid >= m && tid < span) sm.spl[tid] = KeyTraits<I>::sentinel();
+    if (keep) sm.ct.spl[rank] = cand;
     if (tid < nb) sm.cnt[tid] = 0;
+    if (tid == 0) sm.next_bucket = 0;
     // 2. the range into registers, striped and coalesced (only now, so the
     //    sample network above does not hold them live)
     K x[IPT];
@@ -188,15 +185,14 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         }
     }
     __syncthreads();
-    if (tid >= 1 && tid < span) sm.tree[tid] = eytz_node<6>(sm.spl, tid, m);
-    __syncthreads();
+    const CellParams<U> cp = ct_build<kFinNT>(sm.ct, m);  // ends with a barrier
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
     unsigned br[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
         if (p < len) {
-            const unsigned b = cls_eytz<6>(R::to(x[j]), sm.tree, sm.spl, m);
+            const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(x[j]));
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
     }
@@ -222,8 +218,14 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     __syncthreads();
     // 6. warps sort the range buckets in place; equal-to-pivot buckets are
     //    final; oversize buckets are re-queued (written out unsorted below)
+    //    (range buckets 0, 2, .., 2m handed out dynamically: sizes vary)
     const unsigned wmax = min(leaf, kWarpSortMax);
-    for (unsigned b = 2 * warp; b < nb; b += 2 * NW) {
+    for (;;) {
+        unsigned j = 0;
+        if (lane == 0) j = atomicAdd(&sm.next_bucket, 1u);
+        j = __shfl_sync(0xffffffffu, j, 0);
+        if (j > m) break;
+        const unsigned b = 2 * j;
         const unsigned lo = sm.loc[b], c = sm.loc[b + 1] - lo;
         if (c < 2) continue;
         if (c <= wmax) {

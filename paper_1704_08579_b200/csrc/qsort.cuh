@@ -154,11 +154,14 @@ constexpr int kLutBits = 13;  // 8192 cells
 // is classified with one table load and, only when splitters share its
 // cell, a search over those few.  Replaces the 8-level tree search (one
 // dependent shared-memory load per level) of the global levels.
-template <typename U>
-struct CellTable {
-    U spl[256];
-    unsigned short lut[1 << kLutBits];
+template <typename U, int NSPL, int LB>
+struct CellTableT {
+    static constexpr int kBits = LB;
+    U spl[NSPL];
+    unsigned short lut[1 << LB];
 };
+template <typename U>
+using CellTable = CellTableT<U, 256, kLutBits>;
 template <typename U>
 struct CellParams {
     U lo, hi;
@@ -181,12 +184,21 @@ __device__ __forceinline__ unsigned lower_bound_u(const U* a, unsigned lo, unsig
 
 // Load m (>= 1) sorted splitters from the pool and build the table.  All
 // threads of the CTA must call it; contains barriers.
+template <int NT, typename U, int NSPL, int LB>
+__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m);
+
 template <typename K, int NT>
 __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U>& ct, const K* spl_pool,
                                                    unsigned off, unsigned m) {
-    using U = typename OKey<K>::U;
     for (unsigned i = threadIdx.x; i < m; i += NT) ct.spl[i] = OKey<K>::of(spl_pool[off + i]);
     __syncthreads();
+    return ct_build<NT>(ct, m);
+}
+
+// Build the lookup table of a table whose m (>= 1) sorted splitters are
+// already in ct.spl (visible to all threads).  Ends with a barrier.
+template <int NT, typename U, int NSPL, int LB>
+__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m) {
     CellParams<U> p;
     p.m = m;
     p.lo = ct.spl[0];
@@ -194,7 +206,7 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
     const U range = p.hi - p.lo;
     const unsigned bits = range == 0 ? 0u : (unsigned)(8 * sizeof(U)) - (sizeof(U) == 8 ? __clzll((long long)range)
                                                                                       : __clz((int)range));
-    p.shift = bits > kLutBits ? bits - kLutBits : 0u;
+    p.shift = bits > LB ? bits - LB : 0u;
     const unsigned ncell = (unsigned)(range >> p.shift) + 1;
     p.ncell = ncell;
     for (unsigned c = threadIdx.x; c < ncell; c += NT) {
@@ -212,8 +224,8 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
 // lists contain lo / hi, so no separate branches are needed.  Fast path (no
 // splitter inside the key's cell): one table load, no search, and no
 // equality test (no splitter can equal the key).
-template <typename U>
-__device__ __forceinline__ unsigned ct_classify(const CellTable<U>& ct, const CellParams<U>& p, U x) {
+template <typename U, int NSPL, int LB>
+__device__ __forceinline__ unsigned ct_classify(const CellTableT<U, NSPL, LB>& ct, const CellParams<U>& p, U x) {
     const U d = x > p.lo ? x - p.lo : (U)0;
     const U c64 = d >> p.shift;
     const unsigned c = c64 < (U)p.ncell ? (unsigned)c64 : p.ncell - 1;
