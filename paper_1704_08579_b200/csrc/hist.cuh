@@ -1,0 +1,101 @@
+// hist.cuh -- the partition level's histogram pass, TMA-pipelined.
+//
+// Persistent CTAs each own a contiguous chunk of the level's 4096-element
+// tiles (consecutive tiles share a segment, so the segment's cell table is
+// built once per CTA and segment).  Tiles stream into a 3-stage shared
+// memory ring with 1-D bulk copies (cp.async.bulk, completion on an
+// mbarrier) issued two tiles ahead by one thread, so HBM reads overlap the
+// classification of the current tile without holding registers.  Each
+// element is classified into one of 2m+1 buckets (ranges and equal-to-pivot
+// buckets) and counted in a shared histogram that is flushed to the
+// segment's global histogram once per (CTA, segment).
+#pragma once
+
+#include "common.cuh"
+#include "qsort.cuh"
+#include "tma.cuh"
+
+namespace vx {
+
+constexpr int kHistStages = 3;
+
+template <typename K>
+constexpr unsigned hist_stage_bytes() {
+    return (unsigned)(qs_tile<K>() * sizeof(K) + 16);
+}
+template <typename K>
+constexpr unsigned hist_smem_bytes() {
+    return kHistStages * ((hist_stage_bytes<K>() + 127) / 128 * 128);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
+                                                        const Ctl* __restrict__ ctl,
+                                                        const unsigned* __restrict__ tile_owner,
+                                                        const K* __restrict__ spl_pool,
+                                                        unsigned long long* __restrict__ bkt_pool) {
+    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
+    constexpr unsigned BUF = (hist_stage_bytes<K>() + 127) / 128 * 128;
+    using U = typename OKey<K>::U;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ CellTable<U> s_ct;
+    __shared__ unsigned s_hist[kMaxBkt + 1];
+    __shared__ __align__(8) uint64_t s_bar[kHistStages];
+    __shared__ BulkTile s_meta[kHistStages];
+
+    const unsigned ntiles = ctl->tile_ctr;
+    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
+    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
+    if (t0 >= t1) return;
+    const unsigned tid = threadIdx.x;
+
+    auto issue = [&](unsigned t, unsigned stage) {  // one thread
+        const TileGeo g = tile_geo<TILE>(t, tile_owner, segs);
+        BulkTile bt = issue_tile<K>(reinterpret_cast<char*>(smem_raw) + stage * BUF, src, g.base, g.tn,
+                                    &s_bar[stage]);
+        bt.seg = g.seg;
+        s_meta[stage] = bt;
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kHistStages; ++s) mbar_init(&s_bar[s], 1);
+        fence_mbar_init();
+        for (unsigned j = 0; j + 1 < kHistStages && t0 + j < t1; ++j) issue(t0 + j, j);
+    }
+    __syncthreads();
+
+    unsigned cur = 0xffffffffu, bkt_off = 0;
+    CellParams<U> cp{};
+    for (unsigned t = t0; t < t1; ++t) {
+        const unsigned j = t - t0, stage = j % kHistStages, par = (j / kHistStages) & 1;
+        if (tid == 0 && t + kHistStages - 1 < t1) issue(t + kHistStages - 1, (j + kHistStages - 1) % kHistStages);
+        const BulkTile bt = s_meta[stage];
+        if (bt.seg != cur) {
+            // flush the previous segment's counts, build the new table
+            __syncthreads();
+            if (cur != 0xffffffffu)
+                for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT)
+                    if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+            cur = bt.seg;
+            const Seg sg = segs[bt.seg];
+            bkt_off = sg.bkt_off;
+            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);  // barriers inside
+            for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
+            __syncthreads();
+        }
+        mbar_wait(&s_bar[stage], par);
+        const char* buf = reinterpret_cast<const char*>(smem_raw) + stage * BUF;
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+            const unsigned idx = i * kQsNT + tid;
+            if (idx < bt.tn) {
+                const K x = tile_get<K>(buf, bt, src, idx);
+                atomicAdd(&s_hist[ct_classify(s_ct, cp, OKey<K>::of(x))], 1u);
+            }
+        }
+        __syncthreads();  // stage consumed: it is re-filled next iteration
+    }
+    for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT)
+        if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+}
+
+}  // namespace vx

@@ -397,64 +397,6 @@ __device__ __forceinline__ void load_tile(T (&x)[IPT], const T* src, const TileG
     }
 }
 
-// ------------------------------------------------------------ hist
-template <typename K>
-__global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
-                                                        const Ctl* __restrict__ ctl, const unsigned* __restrict__ tile_owner,
-                                                        const K* __restrict__ spl_pool,
-                                                        unsigned long long* __restrict__ bkt_pool) {
-    constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    using U = typename OKey<K>::U;
-    __shared__ CellTable<U> s_ct;
-    __shared__ unsigned s_hist[kMaxBkt + 1];
-    const unsigned ntiles = ctl->tile_ctr;
-    unsigned cur = 0xffffffffu, bkt_off = 0;
-    CellParams<U> cp{};
-    // contiguous chunk of tiles per CTA: consecutive tiles share a segment,
-    // so its classification table is built once per (CTA, segment)
-    const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
-    const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
-    if (t0 >= t1) return;
-    // register double buffering: tile t+1 is in flight while t is classified
-    TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
-    K xs[IPT];
-    load_tile<K, IPT>(xs, src, g);
-    for (unsigned t = t0; t < t1; ++t) {
-        TileGeo gn{};
-        K ys[IPT];
-        if (t + 1 < t1) {
-            gn = tile_geo<TILE>(t + 1, tile_owner, segs);
-            load_tile<K, IPT>(ys, src, gn);
-        }
-        if (g.seg != cur) {
-            // the smem histogram accumulates over all of this CTA's tiles of
-            // one segment and is flushed once per (CTA, segment)
-            __syncthreads();
-            if (cur != 0xffffffffu)
-                for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT)
-                    if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
-            cur = g.seg;
-            const Seg sg = segs[g.seg];
-            bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);  // syncs inside
-            for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
-            __syncthreads();
-        }
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const unsigned idx = i * kQsNT + threadIdx.x;
-            const unsigned b = ct_classify(s_ct, cp, OKey<K>::of(xs[i]));
-            if (idx < g.tn) atomicAdd(&s_hist[b], 1u);
-        }
-#pragma unroll
-        for (int i = 0; i < IPT; ++i) xs[i] = ys[i];
-        g = gn;
-    }
-    __syncthreads();
-    for (unsigned b = threadIdx.x; b < 2 * cp.m + 1; b += kQsNT)
-        if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
-}
-
 // ------------------------------------------------------------ emit
 // Exclusive scan of one u64 per thread over a CTA.
 template <int NT>

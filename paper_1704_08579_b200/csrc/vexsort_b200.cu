@@ -16,6 +16,7 @@
 #include "qsort.cuh"
 #include "finish.cuh"
 #include "scatter.cuh"
+#include "hist.cuh"
 
 using namespace vx;
 
@@ -199,7 +200,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     const unsigned leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
 
     const int sms = num_sms();
-    static int occ_hist = prepare(qs_hist_kernel<K>, kQsNT, 0);
+    static int occ_hist = prepare(qs_hist_kernel<K>, kQsNT, hist_smem_bytes<K>());
     static int occ_scat = prepare(qs_scatter_kernel<K, V>, kQsNT, sizeof(ScatterPipeSmem<K, V>));
     static int occ_fin = prepare(qs_finish_kernel<K, V>, kFinNT, sizeof(FinSmem<K, V>));
     const int g_hist = sms * occ_hist, g_scat = sms * occ_scat, g_fin = sms * occ_fin;
@@ -242,7 +243,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             VX_LAUNCHED();
             {
                 Launch l(KC_HIST, st);
-                qs_hist_kernel<K><<<g_hist, kQsNT, 0, st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
+                qs_hist_kernel<K><<<g_hist, kQsNT, hist_smem_bytes<K>(), st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
             }
             VX_LAUNCHED();
             {
