@@ -100,7 +100,7 @@ __device__ __forceinline__ unsigned long long lookback_excl(unsigned long long* 
 // kin/vin -> kout/vout; n elements; `state` holds ntiles zeroed descriptors,
 // `counter` a zeroed tile ticket; *d_split receives count(x <= pivot).
 template <typename K, typename V, int NT, int IPT, bool VEC>
-__global__ void __launch_bounds__(NT, 3) partition2_kernel(const K* __restrict__ kin, const V* __restrict__ vin,
+__global__ void __launch_bounds__(NT) partition2_kernel(const K* __restrict__ kin, const V* __restrict__ vin,
                                                         K* __restrict__ kout, V* __restrict__ vout, uint64_t n,
                                                         K pivot, unsigned long long* __restrict__ state,
                                                         unsigned* __restrict__ counter,
@@ -113,8 +113,7 @@ __global__ void __launch_bounds__(NT, 3) partition2_kernel(const K* __restrict__
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* sk = reinterpret_cast<K*>(smem_raw);
     V* sv = reinterpret_cast<V*>(smem_raw + sizeof(K) * T);
-    __shared__ unsigned s_cnt[IPT * (NT / 32)];  // per (item, warp): lows | highs << 16
-    __shared__ unsigned s_tot;
+    __shared__ unsigned s_scan[NT / 32 + 1];
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_excl;
 
@@ -157,45 +156,20 @@ __global__ void __launch_bounds__(NT, 3) partition2_kernel(const K* __restrict__
         }
     }
 
-    // classify: x <= pivot goes left (ordered compare: NaN is "high").
-    // Ranks come from warp ballots in (item, warp, lane) order, so the lanes
-    // of a warp stage one item into consecutive shared-memory slots
-    // (conflict-free) instead of each thread walking its own run.
-    constexpr int NW = NT / 32;
-    const unsigned lane = tid & 31, warp = tid >> 5;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    unsigned lowb[IPT], valb[IPT];
+    // classify: x <= pivot goes left (ordered compare: NaN is "high")
+    unsigned lowmask = 0;
 #pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-        const bool va = (valid >> i) & 1u;
-        lowb[i] = __ballot_sync(0xffffffffu, va && (k[i] <= pivot));
-        valb[i] = __ballot_sync(0xffffffffu, va);
-        if (lane == 0) s_cnt[i * NW + warp] = __popc(lowb[i]) | ((__popc(valb[i]) - __popc(lowb[i])) << 16);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        // exclusive scan of the IPT*NW (lows | highs<<16) entries, 4 per lane
-        constexpr int PER = IPT * NW / 32;
-        static_assert(IPT * NW % 32 == 0, "scan layout");
-        unsigned e[PER], sum = 0;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            e[q] = s_cnt[lane * PER + q];
-            sum += e[q];
-        }
-        const unsigned inc = warp_incl_scan(sum);
-        unsigned run = inc - sum;
-#pragma unroll
-        for (int q = 0; q < PER; ++q) {
-            s_cnt[lane * PER + q] = run;
-            run += e[q];
-        }
-        if (lane == 31) s_tot = inc;
-    }
-    __syncthreads();
-    const unsigned L_t = s_tot & 0xffffu, H_t = s_tot >> 16, N_t = L_t + H_t;
+    for (int i = 0; i < IPT; ++i)
+        if (((valid >> i) & 1u) && (k[i] <= pivot)) lowmask |= 1u << i;
+    const unsigned nlow = __popc(lowmask), nval = __popc(valid);
 
-    if (warp == 0) {
+    unsigned total;
+    const unsigned packed = block_excl_scan<NT>(nlow | (nval << 16), s_scan, &total);
+    const unsigned L_t = total & 0xffffu, N_t = total >> 16, H_t = N_t - L_t;
+    unsigned rl = packed & 0xffffu;
+    unsigned rh = L_t + ((packed >> 16) - rl);
+
+    if (tid < 32) {
         const unsigned long long ex = lookback_excl(state, tile, L_t);
         if (tid == 0) s_excl = ex;
     }
@@ -204,10 +178,7 @@ __global__ void __launch_bounds__(NT, 3) partition2_kernel(const K* __restrict__
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
         if ((valid >> i) & 1u) {
-            const unsigned pre = s_cnt[i * NW + warp];
-            const bool lo = (lowb[i] >> lane) & 1u;
-            const unsigned slot = lo ? (pre & 0xffffu) + __popc(lowb[i] & lt_mask)
-                                     : L_t + (pre >> 16) + __popc(valb[i] & ~lowb[i] & lt_mask);
+            const unsigned slot = ((lowmask >> i) & 1u) ? rl++ : rh++;
             sk[slot] = k[i];
             if constexpr (KV) sv[slot] = v[i];
         }
