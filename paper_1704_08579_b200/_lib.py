@@ -16,7 +16,8 @@ __all__ = ["BackendUnavailable", "lib", "check", "lib_path", "VX_I32", "VX_F64",
 
 VX_I32, VX_F64 = 0, 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libvexsort_b200.so")
+# VEXSORT_B200_LIB overrides the library path (tuning experiments only)
+_SO = os.environ.get("VEXSORT_B200_LIB") or os.path.join(_HERE, "libvexsort_b200.so")
 
 
 class BackendUnavailable(RuntimeError):

@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     constexpr unsigned BUF = (hist_stage_bytes<K>() + 127) / 128 * 128;
     using U = typename OKey<K>::U;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellTable<U> s_ct;
     __shared__ unsigned s_hist[kMaxBkt + 1];
     __shared__ __align__(8) uint64_t s_bar[kHistStages];

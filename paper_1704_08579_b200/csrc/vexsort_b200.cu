@@ -290,7 +290,13 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
 
 // -------------------------------------------------------------- partition
 template <typename K>
-struct PartCfg { static constexpr int NT = 256, IPT = 16; };
+#ifndef VX_PART_NT
+#define VX_PART_NT 512
+#endif
+#ifndef VX_PART_IPT
+#define VX_PART_IPT 16
+#endif
+struct PartCfg { static constexpr int NT = VX_PART_NT, IPT = VX_PART_IPT; };
 
 template <typename K, typename V>
 int run_partition(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, K pivot, int64_t* d_split, void* ws,
@@ -528,7 +534,7 @@ int vx_profile_read(int64_t* launches, double* ms, uint64_t* elems, int nclass) 
 
 size_t vx_partition_workspace_bytes(int dtype, int64_t n) {
     (void)dtype;
-    const uint64_t T = 256 * 16;
+    const uint64_t T = VX_PART_NT * VX_PART_IPT;
     return align_up(((uint64_t)n + T - 1) / T * 8) + 256;
 }
 
