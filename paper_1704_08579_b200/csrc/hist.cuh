@@ -29,7 +29,7 @@ constexpr unsigned hist_smem_bytes() {
 }
 
 template <typename K>
-__global__ void __launch_bounds__(kQsNT, 2) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
+__global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
                                                         const Ctl* __restrict__ ctl,
                                                         const unsigned* __restrict__ tile_owner,
                                                         const K* __restrict__ spl_pool,

@@ -38,7 +38,11 @@ namespace vx {
 
 constexpr int kMaxSplit = 255;                 // pivots per segment (level)
 constexpr int kMaxBkt = 2 * kMaxSplit + 1;     // 511 buckets
-constexpr int kQsNT = 512;                     // tile-kernel threads
+#ifndef VX_QS_NT
+#define VX_QS_NT 512
+#endif
+constexpr int kQsNT = VX_QS_NT;                // tile-kernel threads (tile = kQsNT * 8)
+constexpr int kQsMinBlocks = 1024 / kQsNT;
 constexpr int kPlanNT = 512;                   // plan / emit threads
 constexpr int kFinNT = 512;                    // finish-kernel threads
 constexpr int kMaxSample = 4096;
@@ -616,7 +620,7 @@ __global__ void bp_scan_kernel(const unsigned long long* __restrict__ counts, un
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQsNT, 2) bp_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+__global__ void __launch_bounds__(kQsNT, kQsMinBlocks) bp_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t n,
                                                            uint64_t gofs, const K* __restrict__ spk,
                                                            const uint64_t* __restrict__ spi, unsigned m,

@@ -45,7 +45,7 @@ __device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K,
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQsNT, 2) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+__global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v,
                                                            const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
                                                            const unsigned* __restrict__ tile_owner,
