@@ -35,6 +35,7 @@ import argparse
 import ctypes
 import json
 import os
+import shutil
 import statistics
 import subprocess
 import sys
@@ -95,9 +96,12 @@ class ClockSampler:
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50", "-i",
-                 str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            cmd = ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "50", "-i",
+                   str(self.idx)]
+            if shutil.which("stdbuf"):  # line-buffer the pipe so short regions still yield samples
+                cmd = ["stdbuf", "-oL"] + cmd
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.2)  # let the sampler start before the timed region
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -110,6 +114,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.12)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -377,8 +382,10 @@ def run_e2e(args, spec, vx, L, src, vals, dev, rank, world, units, extra):
             d = host.to(dev, non_blocking=True)
             if kind == "sharded":
                 out = vx.sharded_sort(d)
-                res_h = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-                res_h.copy_(out, non_blocking=True)
+                if "res_h" not in extra or extra["res_h"].numel() < out.numel():
+                    torch.cuda.synchronize()  # (re)allocate outside the steady state
+                    extra["res_h"] = torch.empty(2 * out.numel(), dtype=out.dtype, pin_memory=True)
+                extra["res_h"][: out.numel()].copy_(out, non_blocking=True)
                 d2h = out.numel() * out.element_size()
             else:  # segments, in place: offsets travel with the values
                 offs = extra["offs_host"].to(dev, non_blocking=True)
