@@ -413,10 +413,17 @@ def cpu_sample(spec, src=None, n_sample=None):
     kind = spec["kind"]
     if kind in ("sort", "sharded"):
         n = n_sample or (1 << 24)
+        note = ""
+        if spec.get("dist", "uniform") != "uniform":
+            # the reference's median-of-3 quicksort is quadratic on sorted /
+            # reverse / few-unique inputs (SURVEY.md section 0 finding 5):
+            # only a small sample is feasible
+            n = min(n, 1 << 16)
+            note = " (reference is quadratic on this distribution; full n infeasible)"
         if src is not None:
-            return src[:n].cpu().numpy().copy(), f"first 2^{n.bit_length()-1} elements of the device input"
+            return src[:n].cpu().numpy().copy(), f"first 2^{n.bit_length()-1} elements of the device input{note}"
         dt = np.int32 if spec["dtype"] == "i32" else np.float64
-        return inputs.c5_input(dt, spec["dist"], n=n * 64 // 64), f"2^{n.bit_length()-1}-element C5 input"
+        return inputs.c5_input(dt, spec["dist"], n=n), f"2^{n.bit_length()-1}-element C5 input{note}"
     if kind == "kv":
         n = n_sample or (1 << 22)
         k, v = inputs.c4_input(n=n)
