@@ -191,15 +191,8 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
-        const bool va = p < len;
-        const unsigned b = va ? ct_classify(sm.ct, cp, OKey<K>::of(x[j])) : 0u;
-        // one atomic per warp when the whole warp falls in one bucket
-        const unsigned bl = __shfl_sync(0xffffffffu, b, 0);
-        if (__all_sync(0xffffffffu, va && b == bl)) {
-            unsigned base = 0;
-            if (lane == 0) base = atomicAdd(&sm.cnt[bl], 32u);
-            br[j] = (b << 16) | (__shfl_sync(0xffffffffu, base, 0) + lane);
-        } else if (va) {
+        if (p < len) {
+            const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(x[j]));
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
     }

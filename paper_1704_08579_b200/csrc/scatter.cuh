@@ -91,21 +91,10 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         moved += g.tn;
         // classify + rank: (bucket << 16) | rank within the tile
         unsigned br[IPT];
-        const unsigned lane = threadIdx.x & 31;
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
-            const bool va = i * kQsNT + threadIdx.x < g.tn;
-            // whole warp in one bucket (sorted / few-unique inputs): one atomic
-            // for the warp instead of 32 serialised ones on the same address
-            const unsigned bl = __shfl_sync(0xffffffffu, b, 0);
-            if (__all_sync(0xffffffffu, va && b == bl)) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&sm.cnt[bl], 32u);
-                br[i] = (b << 16) | (__shfl_sync(0xffffffffu, base, 0) + lane);
-            } else {
-                br[i] = va ? ((b << 16) | atomicAdd(&sm.cnt[b], 1u)) : 0xffffffffu;
-            }
+            br[i] = (i * kQsNT + threadIdx.x < g.tn) ? ((b << 16) | atomicAdd(&sm.cnt[b], 1u)) : 0xffffffffu;
         }
         __syncthreads();
         // bucket offsets in the tile (2 buckets per thread) + run reservations
