@@ -122,14 +122,40 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     const unsigned tid = threadIdx.x, lane = tid & 31;
 
     // 1. stratified sample read straight from global, sorted by warp 0
-    const unsigned target = max(2u, min(112u, leaf * 7 / 16));
+#ifndef VX_FIN_TARGET
+#define VX_FIN_TARGET 112
+#endif
+    const unsigned target = max(2u, min((unsigned)VX_FIN_TARGET, leaf * 7 / 16));
     const unsigned mt = max(1u, min((unsigned)kFinMaxSplit, len / target));
-    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(8 * (mt + 1))));
+    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(6 * (mt + 1))));
+    // the range into registers first, striped and coalesced
+    K x[IPT];
+    V y[IPT];
+#pragma unroll
+    for (int j = 0; j < IPT; ++j) {
+        const unsigned p = j * kFinNT + tid;
+        if (p < len) {
+            x[j] = ld_stream(src_k + start + p);
+            if constexpr (KV) y[j] = ld_stream(src_v + start + p);
+        }
+    }
     if (tid < S) {
-        const unsigned stride = max(1u, len / S);
         const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
-        const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
-        sm.samp[tid] = OKey<K>::of(src_k[start + q]);
+        if (len >= 2 * kFinNT) {
+            // sample from registers: column tid, a hashed row -> no extra reads
+            const unsigned rows = (len + kFinNT - 1) / kFinNT;
+            unsigned r = (unsigned)(h % rows);
+            if (r * kFinNT + tid >= len) --r;
+            K v = x[0];
+#pragma unroll
+            for (int j = 1; j < IPT; ++j)
+                if ((unsigned)j == r) v = x[j];
+            sm.samp[tid] = OKey<K>::of(v);
+        } else {
+            const unsigned stride = max(1u, len / S);
+            const unsigned q = min(len - 1, (unsigned)(((uint64_t)tid * len) / S) + (unsigned)(h % stride));
+            sm.samp[tid] = OKey<K>::of(src_k[start + q]);
+        }
     }
     __syncthreads();
     // up to 4 warps sort 128-sample chunks in registers, then the chunks are
@@ -172,18 +198,6 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     if (keep) sm.ct.spl[rank] = cand;
     if (tid < nb) sm.cnt[tid] = 0;
     if (tid == 0) sm.next_bucket = 0;
-    // 2. the range into registers, striped and coalesced (only now, so the
-    //    sample network above does not hold them live)
-    K x[IPT];
-    V y[IPT];
-#pragma unroll
-    for (int j = 0; j < IPT; ++j) {
-        const unsigned p = j * kFinNT + tid;
-        if (p < len) {
-            x[j] = ld_stream(src_k + start + p);
-            if constexpr (KV) y[j] = ld_stream(src_v + start + p);
-        }
-    }
     __syncthreads();
     const CellParams<U> cp = ct_build<kFinNT>(sm.ct, m);  // ends with a barrier
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
