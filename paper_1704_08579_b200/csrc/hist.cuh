@@ -17,7 +17,10 @@
 
 namespace vx {
 
-constexpr int kHistStages = 3;
+// TMA ring depth: 3 x 16 KB for int32 tiles, 2 x 32 KB for float64 (so two
+// CTAs still fit on an SM)
+template <typename K>
+constexpr int hist_stages() { return sizeof(K) == 4 ? 3 : 2; }
 
 template <typename K>
 constexpr unsigned hist_stage_bytes() {
@@ -25,7 +28,7 @@ constexpr unsigned hist_stage_bytes() {
 }
 template <typename K>
 constexpr unsigned hist_smem_bytes() {
-    return kHistStages * ((hist_stage_bytes<K>() + 127) / 128 * 128);
+    return hist_stages<K>() * ((hist_stage_bytes<K>() + 127) / 128 * 128);
 }
 
 template <typename K>
@@ -36,6 +39,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                                                         unsigned long long* __restrict__ bkt_pool) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     constexpr unsigned BUF = (hist_stage_bytes<K>() + 127) / 128 * 128;
+    constexpr int kHistStages = hist_stages<K>();
     using U = typename OKey<K>::U;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellTable<U> s_ct;
