@@ -28,8 +28,9 @@ namespace vx {
 
 __device__ __forceinline__ int32_t kmin(int32_t a, int32_t b) { return min(a, b); }
 __device__ __forceinline__ int32_t kmax(int32_t a, int32_t b) { return max(a, b); }
-__device__ __forceinline__ double kmin(double a, double b) { return fmin(a, b); }
-__device__ __forceinline__ double kmax(double a, double b) { return fmax(a, b); }
+// plain ordered compares (NaN unsupported): DSETP + selects, no NaN fix-ups
+__device__ __forceinline__ double kmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double kmax(double a, double b) { return b < a ? a : b; }
 __device__ __forceinline__ uint32_t kmin(uint32_t a, uint32_t b) { return min(a, b); }
 __device__ __forceinline__ uint32_t kmax(uint32_t a, uint32_t b) { return max(a, b); }
 __device__ __forceinline__ uint64_t kmin(uint64_t a, uint64_t b) { return a < b ? a : b; }

@@ -146,7 +146,7 @@ struct OKey<int32_t> {
 template <>
 struct OKey<double> {
     using U = uint64_t;
-    __device__ __forceinline__ static U of(double k) { return KeyRep<double>::to(k); }
+    __device__ __forceinline__ static U of(double k) { return f64_to_ord(k); }
 };
 
 constexpr int kLutBits = 13;  // 8192 cells
