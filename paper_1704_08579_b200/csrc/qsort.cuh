@@ -51,7 +51,10 @@ constexpr uint32_t kCopyChunk = 16384;
 constexpr int kMaxLevels = 48;
 
 template <typename K>
-struct QsTile { static constexpr int IPT = 8; };    // 4096 elements per tile
+#ifndef VX_QS_IPT
+#define VX_QS_IPT 8
+#endif
+struct QsTile { static constexpr int IPT = VX_QS_IPT; };  // 4096-element tiles by default
 template <typename K>
 constexpr int qs_tile() { return kQsNT * QsTile<K>::IPT; }
 
