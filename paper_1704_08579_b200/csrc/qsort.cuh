@@ -85,57 +85,6 @@ struct Ctl {
 enum : unsigned { kErrCapacity = 1, kErrTooLong = 2 };
 
 // ------------------------------------------------------------ classifiers
-// Equality-bucket classifier: bucket = 2*lb + (x == spl[lb]), lb = #{spl < x}.
-// Branch-free lower bound over a pow2-padded splitter table (padding is the
-// sentinel, which is never < x).
-template <typename K>
-__device__ __forceinline__ unsigned cls_eq(K x, const K* spl, unsigned m, unsigned span) {
-    unsigned pos = 0;
-    for (unsigned half = span >> 1; half >= 1; half >>= 1)
-        if (spl[pos + half - 1] < x) pos += half;
-    // pos is now #{spl[i] < x} restricted to span; equality check
-    const unsigned eq = (pos < m) && !(x < spl[pos]);
-    return 2 * pos + eq;
-}
-
-// Same classifier over a table padded (with the sentinel) to 2^LOG entries:
-// a fixed, fully unrolled search, so a thread's independent elements
-// interleave their shared-memory loads instead of serialising on latency.
-template <int LOG, typename K>
-__device__ __forceinline__ unsigned cls_eq_u(K x, const K* spl, unsigned m) {
-    unsigned pos = 0;
-#pragma unroll
-    for (int h = LOG - 1; h >= 0; --h) {
-        const unsigned half = 1u << h;
-        pos += (spl[pos + half - 1] < x) ? half : 0u;
-    }
-    return 2 * pos + (unsigned)((pos < m) & (spl[pos] == x));
-}
-
-// Same classification with the splitters in BFS (Eytzinger) order: the nodes
-// visited at depth d all lie in tree[2^d, 2^(d+1)), consecutive words, so a
-// warp's lanes hit distinct banks on the first five levels (a plain sorted
-// array sends every probe of the upper levels to the same bank).  `sorted`
-// is the ordinary splitter array, used for the equality test.
-template <int L, typename K>
-__device__ __forceinline__ unsigned cls_eytz(K x, const K* tree, const K* sorted, unsigned m) {
-    unsigned i = 1;
-#pragma unroll
-    for (int d = 0; d < L; ++d) i = 2 * i + (unsigned)(tree[i] < x);
-    const unsigned lb = i - (1u << L);  // #splitters < x
-    return 2 * lb + (unsigned)((lb < m) & (sorted[lb] == x));
-}
-
-// Build the BFS layout of a sorted table padded to 2^L - 1 entries (sentinel
-// beyond m): node k at depth d holds in-order element
-// ((2*(k - 2^d) + 1) << (L-1-d)) - 1.
-template <int L, typename K>
-__device__ __forceinline__ K eytz_node(const K* sorted, unsigned k, unsigned m) {
-    const unsigned d = 31 - __clz(k);
-    const unsigned pos = ((2 * (k - (1u << d)) + 1) << (L - 1 - d)) - 1;
-    return pos < m ? sorted[pos] : KeyTraits<K>::sentinel();
-}
-
 // ---------------------------------------------------- cell-table classifier
 // Keys as order-preserving unsigned codes: int32 -> uint32 (sign bit
 // flipped), float64 -> the uint64 code of KeyRep<double>.
@@ -154,13 +103,15 @@ struct OKey<double> {
 
 constexpr int kLutBits = 13;  // 8192 cells
 
-// Per-segment classification table: the sorted splitters plus a 4096-cell
+// Per-segment classification table: the sorted splitters plus a 2^LB-cell
 // lookup table over [lo, hi] (the smallest / largest splitter).  Cell c
 // covers codes [lo + c<<shift, lo + (c+1)<<shift); lut[c] packs
-// (#splitters below the cell) | (#splitters inside the cell) << 16, so a key
+// (#splitters below the cell) | (#splitters inside the cell) << 8, so a key
 // is classified with one table load and, only when splitters share its
-// cell, a search over those few.  Replaces the 8-level tree search (one
-// dependent shared-memory load per level) of the global levels.
+// cell, a compare or a short search over those few.  (Measured against a
+// binary search over the sorted splitters -- every upper-level probe lands in
+// the same shared-memory bank -- and an Eytzinger-order search; the table is
+// fewer instructions and conflict-free.)
 template <typename U, int NSPL, int LB>
 struct CellTableT {
     static constexpr int kBits = LB;
@@ -360,20 +311,6 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         for (unsigned t = threadIdx.x; t < ntiles; t += kPlanNT) tile_owner[s_off[2] + t] = s;
         __syncthreads();
     }
-}
-
-// Load one segment's splitters into smem, padded with the sentinel to a pow2
-// span.  Returns the span.
-template <typename K, int NT>
-__device__ __forceinline__ unsigned load_splitters(typename KeyRep<K>::I* s_spl, typename KeyRep<K>::I* s_tree,
-                                                   const K* spl_pool, unsigned off, unsigned m) {
-    using I = typename KeyRep<K>::I;
-    // sorted table padded to 256 with the sentinel, then its BFS layout
-    for (unsigned i = threadIdx.x; i < 256; i += NT)
-        s_spl[i] = i < m ? KeyRep<K>::to(spl_pool[off + i]) : KeyTraits<I>::sentinel();
-    __syncthreads();
-    for (unsigned k = threadIdx.x + 1; k < 256; k += NT) s_tree[k] = eytz_node<8>(s_spl, k, m);
-    return 256;
 }
 
 // ------------------------------------------------------------ tiles
