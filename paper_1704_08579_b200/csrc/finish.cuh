@@ -14,9 +14,12 @@
 //     with a shared-memory atomic, and written bucket-major into a padded
 //     smem buffer (one pad word per 32 makes blocked warp reads conflict-free);
 //   * warps sort the range buckets IN shared memory with the register
-//     bitonic network; buckets above the leaf bound are written out as they
-//     are and re-queued for another finish round (the reference's "partition
-//     again" branch);
+//     bitonic network; for 8-byte keys and pairs (where the network
+//     dominates) many small buckets are cut and adjacent ones packed
+//     greedily into runs of <= 128 slots, so every network runs nearly
+//     full; buckets above the leaf bound are written out as they are and
+//     re-queued for another finish round (the reference's "partition again"
+//     branch);
 //   * the whole range, now sorted, leaves with one coalesced store.
 #pragma once
 
@@ -26,8 +29,16 @@
 
 namespace vx {
 
-constexpr int kFinMaxSplit = 63;
+constexpr int kFinMaxSplit = 255;
 constexpr int kFinMaxBkt = 2 * kFinMaxSplit + 1;
+#ifndef VX_FIN_LUT_BITS
+#define VX_FIN_LUT_BITS 10
+#endif
+#ifndef VX_FIN_GROUP
+#define VX_FIN_GROUP 128
+#endif
+constexpr int kFinLutBits = VX_FIN_LUT_BITS;
+constexpr unsigned kFinGroup = VX_FIN_GROUP;  // adjacent buckets are sorted together up to this many slots
 constexpr int kFinMaxSample = 512;
 constexpr unsigned kWarpSortMax = 256;
 
@@ -43,10 +54,12 @@ struct FinSmem {
     using U = typename OKey<K>::U;  // samples and pivots as order-preserving codes
     U samp[kFinMaxSample];
     U samp2[kFinMaxSample];
-    CellTableT<U, kFinMaxSplit + 1, 9> ct;  // pivots + 512-cell lookup table
-    unsigned next_bucket;
+    CellTableT<U, kFinMaxSplit + 1, kFinLutBits> ct;  // pivots + 1024-cell lookup table
+    unsigned next_bucket, ngrp;
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
+    unsigned short nxt[kFinMaxBkt + 1];  // greedy group successor of each bucket
+    unsigned short grp[kFinMaxBkt + 2];  // group boundaries (bucket ids)
     unsigned scan[kFinNT / 32 + 1];
 };
 
@@ -122,12 +135,21 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     const unsigned tid = threadIdx.x, lane = tid & 31;
 
     // 1. stratified sample read straight from global, sorted by warp 0
-#ifndef VX_FIN_TARGET
-#define VX_FIN_TARGET 112
+    // mean fine-bucket size: small buckets packed into full networks pay off
+    // when the network dominates (8-byte keys, pairs); for 4-byte keys the
+    // extra pivots cost more than the padding they save
+#ifndef VX_FIN_TARGET4
+#define VX_FIN_TARGET4 112
 #endif
-    const unsigned target = max(2u, min((unsigned)VX_FIN_TARGET, leaf * 7 / 16));
+#ifndef VX_FIN_TARGET8
+#define VX_FIN_TARGET8 40
+#endif
+    constexpr bool kGroup = (sizeof(K) + (KV ? sizeof(V) : 0)) > 4;
+    constexpr unsigned kTarget = kGroup ? VX_FIN_TARGET8 : VX_FIN_TARGET4;
+    constexpr unsigned kSampleX = kGroup ? 3 : 6;  // samples per pivot (grouping tolerates uneven buckets)
+    const unsigned target = max(2u, min(kTarget, leaf * 7 / 16));
     const unsigned mt = max(1u, min((unsigned)kFinMaxSplit, len / target));
-    const unsigned S = max(32u, min((unsigned)kFinMaxSample, next_pow2_u32(6 * (mt + 1))));
+    const unsigned S = max(32u, min((unsigned)kFinMaxSample, 2u << (31 - __clz(kSampleX * (mt + 1) - 1))));  // pow2 >= x(mt+1)
     // the range into registers first, striped and coalesced
     K x[IPT];
     V y[IPT];
@@ -197,9 +219,12 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     const unsigned nb = 2 * m + 1;
     if (keep) sm.ct.spl[rank] = cand;
     if (tid < nb) sm.cnt[tid] = 0;
-    if (tid == 0) sm.next_bucket = 0;
+    if (tid == 0) {
+        sm.next_bucket = 0;
+        sm.grp[0] = 0;
+    }
     __syncthreads();
-    const CellParams<U> cp = ct_build<kFinNT>(sm.ct, m);  // ends with a barrier
+    const CellParams<U> cp = ct_build<kFinNT>(sm.ct, m, sm.scan);  // ends with a barrier
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
     unsigned br[IPT];
 #pragma unroll
@@ -230,18 +255,45 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         }
     }
     __syncthreads();
-    // 6. warps sort the range buckets in place; equal-to-pivot buckets are
-    //    final; oversize buckets are re-queued (written out unsorted below)
-    //    (range buckets 0, 2, .., 2m handed out dynamically: sizes vary)
+    // 6. group adjacent buckets greedily into runs of <= G slots (fine
+    //    buckets from many pivots, packed so every warp network runs nearly
+    //    full); a bucket alone above G is sorted with a wider network, or --
+    //    above the leaf bound -- re-queued (written out unsorted below);
+    //    an equal-to-pivot bucket alone is final.
     const unsigned wmax = min(leaf, kWarpSortMax);
+    unsigned ngrp = m + 1;  // without grouping: the m+1 range buckets, one by one
+    if constexpr (kGroup) {
+        const unsigned G = min(wmax, kFinGroup);
+        for (unsigned s = tid; s < nb; s += kFinNT) {
+            // last e in [s+1, nb] with loc[e] - loc[s] <= G (loc is nondecreasing)
+            const unsigned lim = sm.loc[s] + G;
+            unsigned lo = s + 1, hi = nb + 1;
+            while (lo < hi) {
+                const unsigned mid = (lo + hi) >> 1;
+                if (sm.loc[mid] <= lim) lo = mid + 1; else hi = mid;
+            }
+            sm.nxt[s] = (unsigned short)max(lo - 1, s + 1);
+        }
+        __syncthreads();
+        if (tid == 0) {  // the greedy walk itself is serial (one short chain)
+            unsigned s = 0, g = 0;
+            while (s < nb) {
+                s = sm.nxt[s];
+                sm.grp[++g] = (unsigned short)s;
+            }
+            sm.ngrp = g;
+        }
+        __syncthreads();
+        ngrp = sm.ngrp;
+    }
     for (;;) {
         unsigned j = 0;
         if (lane == 0) j = atomicAdd(&sm.next_bucket, 1u);
         j = __shfl_sync(0xffffffffu, j, 0);
-        if (j > m) break;
-        const unsigned b = 2 * j;
-        const unsigned lo = sm.loc[b], c = sm.loc[b + 1] - lo;
-        if (c < 2) continue;
+        if (j >= ngrp) break;
+        const unsigned s = kGroup ? sm.grp[j] : 2 * j, e = kGroup ? sm.grp[j + 1] : 2 * j + 1;
+        const unsigned lo = sm.loc[s], c = sm.loc[e] - lo;
+        if (c < 2 || (e == s + 1 && (s & 1u))) continue;  // trivial, or one equal-to-pivot bucket
         if (c <= wmax) {
             if constexpr (KV) warp_sort_smem<K, V>(sm.b, sm.bv, lo, c);
             else warp_sort_smem<K, V>(sm.b, (V*)nullptr, lo, c);

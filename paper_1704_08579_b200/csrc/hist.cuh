@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellTable<U> s_ct;
     __shared__ unsigned s_hist[kMaxBkt + 1];
+    __shared__ unsigned s_scan[kQsNT / 32 + 1];
     __shared__ __align__(8) uint64_t s_bar[kHistStages];
     __shared__ BulkTile s_meta[kHistStages];
 
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             cur = bt.seg;
             const Seg sg = segs[bt.seg];
             bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m);  // barriers inside
+            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
             for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
             __syncthreads();
         }

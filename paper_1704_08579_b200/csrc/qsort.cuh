@@ -141,22 +141,29 @@ __device__ __forceinline__ unsigned lower_bound_u(const U* a, unsigned lo, unsig
 }
 
 // Load m (>= 1) sorted splitters from the pool and build the table.  All
-// threads of the CTA must call it; contains barriers.
+// threads of the CTA must call it; contains barriers.  `scan` is block-scan
+// scratch (NT/32 + 1 words).
 template <int NT, typename U, int NSPL, int LB>
-__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m);
+__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsigned* scan);
 
 template <typename K, int NT>
 __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U>& ct, const K* spl_pool,
-                                                   unsigned off, unsigned m) {
+                                                   unsigned off, unsigned m, unsigned* scan) {
     for (unsigned i = threadIdx.x; i < m; i += NT) ct.spl[i] = OKey<K>::of(spl_pool[off + i]);
     __syncthreads();
-    return ct_build<NT>(ct, m);
+    return ct_build<NT>(ct, m, scan);
 }
 
-// Build the lookup table of a table whose m (>= 1) sorted splitters are
-// already in ct.spl (visible to all threads).  Ends with a barrier.
+// Build the lookup table of a table whose m (1 <= m <= 255) sorted splitters
+// are already in ct.spl (visible to all threads).  Counting construction:
+// every splitter bumps its cell's count (16-bit halves of the table words),
+// then one block scan over the cells turns counts into "#splitters below the
+// cell" -- no per-cell search.  Ends with a barrier.
 template <int NT, typename U, int NSPL, int LB>
-__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m) {
+__device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsigned* scan) {
+    constexpr int NC = 1 << LB;
+    static_assert(NC >= NT && NC % NT == 0, "cells must cover the CTA evenly");
+    constexpr int CPT = NC / NT;
     CellParams<U> p;
     p.m = m;
     p.lo = ct.spl[0];
@@ -165,13 +172,28 @@ __device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m) {
     const unsigned bits = range == 0 ? 0u : (unsigned)(8 * sizeof(U)) - (sizeof(U) == 8 ? __clzll((long long)range)
                                                                                       : __clz((int)range));
     p.shift = bits > LB ? bits - LB : 0u;
-    const unsigned ncell = (unsigned)(range >> p.shift) + 1;
-    p.ncell = ncell;
-    for (unsigned c = threadIdx.x; c < ncell; c += NT) {
-        const U cmin = p.lo + ((U)c << p.shift);
-        const unsigned lbmin = lower_bound_u(ct.spl, 0, m, cmin);
-        const unsigned lbmax = (c + 1 < ncell) ? lower_bound_u(ct.spl, lbmin, m - lbmin, cmin + ((U)1 << p.shift)) : m;
-        ct.lut[c] = (unsigned short)(lbmin | ((lbmax - lbmin) << 8));  // m <= 255: 8 | 8 bits
+    p.ncell = (unsigned)(range >> p.shift) + 1;
+    unsigned* w = reinterpret_cast<unsigned*>(ct.lut);
+    for (unsigned i = threadIdx.x; i < NC / 2; i += NT) w[i] = 0u;
+    __syncthreads();
+    for (unsigned i = threadIdx.x; i < m; i += NT) {
+        const unsigned c = (unsigned)((ct.spl[i] - p.lo) >> p.shift);
+        atomicAdd(&w[c >> 1], 1u << (16 * (c & 1u)));
+    }
+    __syncthreads();
+    unsigned cnt[CPT], sum = 0;
+    const unsigned c0 = threadIdx.x * CPT;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        cnt[j] = ct.lut[c0 + j];
+        sum += cnt[j];
+    }
+    unsigned tot;
+    unsigned below = block_excl_scan<NT>(sum, scan, &tot);  // ends with a barrier
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+        ct.lut[c0 + j] = (unsigned short)(below | (cnt[j] << 8));  // m <= 255: 8 | 8 bits
+        below += cnt[j];
     }
     __syncthreads();
     return p;

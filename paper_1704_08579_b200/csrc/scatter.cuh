@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
             cur = g.seg;
             const Seg sg = segs[g.seg];
             bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m);  // syncs inside
+            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m, sm.scan);  // syncs inside
         }
         const unsigned nb = 2 * cp.m + 1;
         for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;

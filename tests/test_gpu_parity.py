@@ -585,7 +585,8 @@ def test_profile_counters_report_launches_and_elements():
     el = (ctypes.c_uint64 * 8)()
     assert L.vx_profile_read(la, ms, el, 8) == 8
     assert la[3] >= 1 and la[4] >= 1  # scatter, finish
-    assert el[4] >= (1 << 22)  # every element finished at least once
+    assert el[3] >= (1 << 22)  # the first level moves every element
+    assert el[4] >= (1 << 21)  # most elements end in a finish item
     assert ms[4] > 0.0
 
 
