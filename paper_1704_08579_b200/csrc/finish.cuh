@@ -224,14 +224,14 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         sm.grp[0] = 0;
     }
     __syncthreads();
-    const CellParams<U> cp = ct_build<kFinNT>(sm.ct, m, sm.scan);  // ends with a barrier
+    const CellParams<U> cp = ct_build<kFinNT, false>(sm.ct, m, sm.scan);  // code map (narrow ranges); ends with a barrier
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
     unsigned br[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
         if (p < len) {
-            const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(x[j]));
+            const unsigned b = ct_classify(sm.ct, cp, x[j]);
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
     }

@@ -2,10 +2,12 @@
 //
 // Persistent CTAs each own a contiguous chunk of the level's 4096-element
 // tiles (consecutive tiles share a segment, so the segment's cell table is
-// built once per CTA and segment).  Tiles stream into a 3-stage shared
-// memory ring with 1-D bulk copies (cp.async.bulk, completion on an
-// mbarrier) issued two tiles ahead by one thread, so HBM reads overlap the
-// classification of the current tile without holding registers.  Each
+// built once per CTA and segment).  Tiles stream into a shared memory ring
+// (4 stages for int32) with 1-D bulk copies (cp.async.bulk, completion on an
+// mbarrier) issued NS-1 tiles ahead by one thread, so HBM reads overlap the
+// classification of the current tile without holding registers.  The copy
+// takes the tile's 16-byte aligned window whenever it lies inside the array,
+// so every element is read from shared memory with no edge tests.  Each
 // element is classified into one of 2m+1 buckets (ranges and equal-to-pivot
 // buckets) and counted in a shared histogram that is flushed to the
 // segment's global histogram once per (CTA, segment).
@@ -17,36 +19,45 @@
 
 namespace vx {
 
-// TMA ring depth: 3 x 16 KB for int32 tiles, 2 x 32 KB for float64 (so two
+// TMA ring depth: 4 x 16 KB for int32 tiles, 2 x 32 KB for float64 (so two
 // CTAs still fit on an SM)
+#ifndef VX_HIST_STAGES4
+#define VX_HIST_STAGES4 4
+#endif
 template <typename K>
-constexpr int hist_stages() { return sizeof(K) == 4 ? 3 : 2; }
+constexpr int hist_stages() { return sizeof(K) == 4 ? VX_HIST_STAGES4 : 2; }
 
 template <typename K>
 constexpr unsigned hist_stage_bytes() {
-    return (unsigned)(qs_tile<K>() * sizeof(K) + 16);
+    return (unsigned)(qs_tile<K>() * sizeof(K) + 32);
 }
 template <typename K>
 constexpr unsigned hist_smem_bytes() {
     return hist_stages<K>() * ((hist_stage_bytes<K>() + 127) / 128 * 128);
 }
 
+// Ring protocol: full[s] completes when the bulk copy into stage s landed;
+// empty[s] (count = CTA size) when every thread has consumed it.  Thread 0
+// refills a stage only after its empty phase, so warps drift freely within
+// the ring instead of meeting at a CTA barrier every tile.
 template <typename K>
-__global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* __restrict__ src, const Seg* __restrict__ segs,
+__global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* __restrict__ src, uint64_t n_all,
+                                                        const Seg* __restrict__ segs,
                                                         const Ctl* __restrict__ ctl,
                                                         const unsigned* __restrict__ tile_owner,
                                                         const K* __restrict__ spl_pool,
                                                         unsigned long long* __restrict__ bkt_pool) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     constexpr unsigned BUF = (hist_stage_bytes<K>() + 127) / 128 * 128;
-    constexpr int kHistStages = hist_stages<K>();
+    constexpr int NS = hist_stages<K>();
     using U = typename OKey<K>::U;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ CellTable<U> s_ct;
     __shared__ unsigned s_hist[kMaxBkt + 1];
     __shared__ unsigned s_scan[kQsNT / 32 + 1];
-    __shared__ __align__(8) uint64_t s_bar[kHistStages];
-    __shared__ BulkTile s_meta[kHistStages];
+    __shared__ __align__(8) uint64_t s_full[NS];
+    __shared__ __align__(8) uint64_t s_empty[NS];
+    __shared__ BulkTile s_meta[NS];
 
     const unsigned ntiles = ctl->tile_ctr;
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
@@ -56,23 +67,32 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
 
     auto issue = [&](unsigned t, unsigned stage) {  // one thread
         const TileGeo g = tile_geo<TILE>(t, tile_owner, segs);
-        BulkTile bt = issue_tile<K>(reinterpret_cast<char*>(smem_raw) + stage * BUF, src, g.base, g.tn,
-                                    &s_bar[stage]);
+        BulkTile bt = issue_tile_window<K>(reinterpret_cast<char*>(smem_raw) + stage * BUF, src, n_all, g.base,
+                                           g.tn, &s_full[stage]);
         bt.seg = g.seg;
         s_meta[stage] = bt;
     };
     if (tid == 0) {
-        for (int s = 0; s < kHistStages; ++s) mbar_init(&s_bar[s], 1);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&s_full[s], 1);
+            mbar_init(&s_empty[s], kQsNT);
+        }
         fence_mbar_init();
-        for (unsigned j = 0; j + 1 < kHistStages && t0 + j < t1; ++j) issue(t0 + j, j);
+        for (unsigned j = 0; j + 1 < NS && t0 + j < t1; ++j) issue(t0 + j, j);
     }
     __syncthreads();
 
     unsigned cur = 0xffffffffu, bkt_off = 0;
     CellParams<U> cp{};
+    unsigned stage = 0, par = 0;          // this tile's stage and phase parity
+    unsigned pstage = NS - 1, ppar = 1;   // the previous tile's
     for (unsigned t = t0; t < t1; ++t) {
-        const unsigned j = t - t0, stage = j % kHistStages, par = (j / kHistStages) & 1;
-        if (tid == 0 && t + kHistStages - 1 < t1) issue(t + kHistStages - 1, (j + kHistStages - 1) % kHistStages);
+        if (tid == 0 && t + NS - 1 < t1) {
+            // refill the previous tile's stage once everybody is done with it
+            if (t > t0) mbar_wait(&s_empty[pstage], ppar);
+            issue(t + NS - 1, pstage);
+        }
+        mbar_wait(&s_full[stage], par);
         const BulkTile bt = s_meta[stage];
         if (bt.seg != cur) {
             // flush the previous segment's counts, build the new table
@@ -87,18 +107,31 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
             __syncthreads();
         }
-        mbar_wait(&s_bar[stage], par);
         const char* buf = reinterpret_cast<const char*>(smem_raw) + stage * BUF;
+        if (bt.body == TILE) {  // the whole (full) tile is in shared memory
+            const K* sb = reinterpret_cast<const K*>(buf + bt.shift);
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const unsigned idx = i * kQsNT + tid;
-            if (idx < bt.tn) {
-                const K x = tile_get<K>(buf, bt, src, idx);
-                atomicAdd(&s_hist[ct_classify(s_ct, cp, OKey<K>::of(x))], 1u);
+            for (int i = 0; i < IPT; ++i)
+                atomicAdd(&s_hist[ct_classify(s_ct, cp, sb[i * kQsNT + tid])], 1u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const unsigned idx = i * kQsNT + tid;
+                if (idx < bt.tn) {
+                    const K x = tile_get<K>(buf, bt, src, idx);
+                    atomicAdd(&s_hist[ct_classify(s_ct, cp, x)], 1u);
+                }
             }
         }
-        __syncthreads();  // stage consumed: it is re-filled next iteration
+        mbar_arrive(&s_empty[stage]);
+        pstage = stage;
+        ppar = par;
+        if (++stage == NS) {
+            stage = 0;
+            par ^= 1u;
+        }
     }
+    __syncthreads();
     for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT)
         if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
 }

@@ -120,10 +120,15 @@ struct CellTableT {
 };
 template <typename U>
 using CellTable = CellTableT<U, 256, kLutBits>;
+// Cell map: code-linear (cell = (code - lo) >> shift) or, for float64 keys
+// whose splitters crowd a few code cells (e.g. uniform values spanning
+// several binades), value-linear (cell = (v - vlo) * vscale).  Either map is
+// monotone, which is all the table needs.
 template <typename U>
 struct CellParams {
     U lo, hi;
-    unsigned shift, m, ncell;
+    unsigned shift, m, ncell, vmode;
+    double vlo, vscale;
 };
 
 template <typename U>
@@ -143,7 +148,7 @@ __device__ __forceinline__ unsigned lower_bound_u(const U* a, unsigned lo, unsig
 // Load m (>= 1) sorted splitters from the pool and build the table.  All
 // threads of the CTA must call it; contains barriers.  `scan` is block-scan
 // scratch (NT/32 + 1 words).
-template <int NT, typename U, int NSPL, int LB>
+template <int NT, bool kTryValue = true, typename U, int NSPL, int LB>
 __device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsigned* scan);
 
 template <typename K, int NT>
@@ -154,18 +159,36 @@ __device__ CellParams<typename OKey<K>::U> ct_load(CellTable<typename OKey<K>::U
     return ct_build<NT>(ct, m, scan);
 }
 
+template <typename U>
+__device__ __forceinline__ unsigned cell_code(const CellParams<U>& p, U x) {
+    const U d = x > p.lo ? x - p.lo : (U)0;
+    const U c64 = d >> p.shift;
+    return c64 < (U)p.ncell ? (unsigned)c64 : p.ncell - 1;
+}
+template <typename U>
+__device__ __forceinline__ unsigned cell_val(const CellParams<U>& p, double v) {
+    double t = (v - p.vlo) * p.vscale;  // NaN keys are unsupported (as in the reference)
+    t = t > 0.0 ? t : 0.0;
+    return t < (double)(p.ncell - 1) ? (unsigned)t : p.ncell - 1;
+}
+
 // Build the lookup table of a table whose m (1 <= m <= 255) sorted splitters
 // are already in ct.spl (visible to all threads).  Counting construction:
 // every splitter bumps its cell's count (16-bit halves of the table words),
 // then one block scan over the cells turns counts into "#splitters below the
-// cell" -- no per-cell search.  Ends with a barrier.
-template <int NT, typename U, int NSPL, int LB>
+// cell" -- no per-cell search.  For 64-bit codes (float64 keys) a crowded
+// code map (sum of squared cell counts well above m) is retried value-linear
+// and the less crowded map is kept (kTryValue).  Ends with a barrier.
+template <int NT, bool kTryValue, typename U, int NSPL, int LB>
 __device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsigned* scan) {
     constexpr int NC = 1 << LB;
     static_assert(NC >= NT && NC % NT == 0, "cells must cover the CTA evenly");
     constexpr int CPT = NC / NT;
     CellParams<U> p;
     p.m = m;
+    p.vmode = 0;
+    p.vlo = 0.0;
+    p.vscale = 0.0;
     p.lo = ct.spl[0];
     p.hi = ct.spl[m - 1];
     const U range = p.hi - p.lo;
@@ -174,19 +197,48 @@ __device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsig
     p.shift = bits > LB ? bits - LB : 0u;
     p.ncell = (unsigned)(range >> p.shift) + 1;
     unsigned* w = reinterpret_cast<unsigned*>(ct.lut);
-    for (unsigned i = threadIdx.x; i < NC / 2; i += NT) w[i] = 0u;
-    __syncthreads();
-    for (unsigned i = threadIdx.x; i < m; i += NT) {
-        const unsigned c = (unsigned)((ct.spl[i] - p.lo) >> p.shift);
-        atomicAdd(&w[c >> 1], 1u << (16 * (c & 1u)));
-    }
-    __syncthreads();
-    unsigned cnt[CPT], sum = 0;
     const unsigned c0 = threadIdx.x * CPT;
+    unsigned cnt[CPT], sum = 0, sq = 0;
+    auto count = [&]() {  // per-cell splitter counts of the current map into cnt[]
+        for (unsigned i = threadIdx.x; i < NC / 2; i += NT) w[i] = 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < m; i += NT) {
+            unsigned c;
+            if constexpr (sizeof(U) == 8) c = p.vmode ? cell_val(p, ord_to_f64(ct.spl[i])) : cell_code(p, ct.spl[i]);
+            else c = cell_code(p, ct.spl[i]);
+            atomicAdd(&w[c >> 1], 1u << (16 * (c & 1u)));
+        }
+        __syncthreads();
+        sum = 0;
+        sq = 0;
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) {
-        cnt[j] = ct.lut[c0 + j];
-        sum += cnt[j];
+        for (int j = 0; j < CPT; ++j) {
+            cnt[j] = ct.lut[c0 + j];
+            sum += cnt[j];
+            sq += cnt[j] * cnt[j];
+        }
+    };
+    count();
+    if constexpr (sizeof(U) == 8 && kTryValue) {
+        unsigned sq_code;
+        block_excl_scan<NT>(sq, scan, &sq_code);
+        const double vlo = ord_to_f64(p.lo), vhi = ord_to_f64(p.hi), span = vhi - vlo;
+        if (sq_code > m + m / 8 && span > 0.0 && span <= 1.7e308) {
+            const unsigned code_ncell = p.ncell;
+            p.vmode = 1;
+            p.vlo = vlo;
+            p.vscale = (double)(NC - 1) / span;
+            p.ncell = NC;
+            p.ncell = cell_val(p, vhi) + 1;  // the last cell holds hi
+            count();
+            unsigned sq_val;
+            block_excl_scan<NT>(sq, scan, &sq_val);
+            if (sq_val >= sq_code) {  // no better: back to the code map
+                p.vmode = 0;
+                p.ncell = code_ncell;
+                count();
+            }
+        }
     }
     unsigned tot;
     unsigned below = block_excl_scan<NT>(sum, scan, &tot);  // ends with a barrier
@@ -201,24 +253,43 @@ __device__ CellParams<U> ct_build(CellTableT<U, NSPL, LB>& ct, unsigned m, unsig
 
 // bucket = 2*lb + (x == spl[lb]), lb = #splitters < x (equality buckets odd)
 // Keys below lo / above hi clamp into the first / last cell, whose splitter
-// lists contain lo / hi, so no separate branches are needed.  Fast path (no
-// splitter inside the key's cell): one table load, no search, and no
-// equality test (no splitter can equal the key).
+// lists contain lo / hi, so no separate branches are needed.  With at most
+// one splitter in the key's cell the answer is branch-free: s = spl[lbmin]
+// is that splitter, or -- empty cell -- the first splitter above the cell,
+// which is > x (every reachable empty cell lies below the last cell, so
+// lbmin <= m-1 and s exists).  Only cells holding >= 2 splitters search.
 template <typename U, int NSPL, int LB>
-__device__ __forceinline__ unsigned ct_classify(const CellTableT<U, NSPL, LB>& ct, const CellParams<U>& p, U x) {
-    const U d = x > p.lo ? x - p.lo : (U)0;
-    const U c64 = d >> p.shift;
-    const unsigned c = c64 < (U)p.ncell ? (unsigned)c64 : p.ncell - 1;
+__device__ __forceinline__ unsigned ct_classify_cell(const CellTableT<U, NSPL, LB>& ct, const CellParams<U>& p, U x,
+                                                     unsigned c) {
     const unsigned e = ct.lut[c];
     unsigned lb = e & 0xffu;
+#ifdef VX_CLS_BRANCHY
     const unsigned cnt = e >> 8;
     if (cnt == 0) return 2 * lb;
-    if (cnt == 1) {  // the common slow case: one splitter shares the cell
+    if (cnt == 1) {
         const U s = ct.spl[lb];
         return 2 * (lb + (unsigned)(s < x)) + (unsigned)(s == x);
     }
-    lb = lower_bound_u(ct.spl, lb, cnt, x);
+#else
+    if (e < (2u << 8)) {
+        const U s = ct.spl[lb];
+        return 2 * (lb + (unsigned)(s < x)) + (unsigned)(s == x);
+    }
+#endif
+    lb = lower_bound_u(ct.spl, lb, e >> 8, x);
     return 2 * lb + (unsigned)(lb < p.m && ct.spl[lb] == x);
+}
+
+// classify a key (int32 / float64) against a table built by ct_build
+template <typename K, typename U, int NSPL, int LB>
+__device__ __forceinline__ unsigned ct_classify(const CellTableT<U, NSPL, LB>& ct, const CellParams<U>& p, K key) {
+    const U x = OKey<K>::of(key);
+    if constexpr (sizeof(K) == 8) {
+        const unsigned c = p.vmode ? cell_val(p, (double)key) : cell_code(p, x);
+        return ct_classify_cell(ct, p, x, c);
+    } else {
+        return ct_classify_cell(ct, p, x, cell_code(p, x));
+    }
 }
 
 // (key, global index) classifier for the sharded sort: bucket = number of

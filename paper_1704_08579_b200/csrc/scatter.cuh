@@ -23,12 +23,11 @@ struct ScatterPipeSmem {
         K k[TILE];
         VS v[HasVal<V>::value ? TILE : 1];
         unsigned short b[TILE];
-        unsigned loc[kMaxBkt + 1];
-        unsigned long long gbase[kMaxBkt + 1];
+        unsigned long long delta[kMaxBkt + 1];  // destination of slot j in bucket b: delta[b] + j
         unsigned tn;
     };
     Stage st[2];
-    unsigned cnt[kMaxBkt + 1];
+    unsigned cnt[2][kMaxBkt + 1];  // per-tile counts, then (in place) bucket offsets; double-buffered
     CellTable<typename OKey<K>::U> ct;
     unsigned scan[kQsNT / 32 + 1];
 };
@@ -37,8 +36,7 @@ template <typename K, typename V>
 __device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K, V>::Stage& s, K* dst_k, V* dst_v) {
     constexpr bool KV = HasVal<V>::value;
     for (unsigned j = threadIdx.x; j < s.tn; j += kQsNT) {
-        const unsigned b = s.b[j];
-        const unsigned long long pos = s.gbase[b] + (j - s.loc[b]);
+        const unsigned long long pos = s.delta[s.b[j]] + j;
         dst_k[pos] = s.k[j];
         if constexpr (KV) dst_v[pos] = s.v[j];
     }
@@ -60,6 +58,9 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
     if (t0 >= t1) return;
+    const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;  // the two buckets this thread scans / reserves
+    const bool owner = b1 <= (unsigned)kMaxBkt;        // threads past the bucket range own none
+    if (owner) sm.cnt[0][b0] = sm.cnt[0][b1] = sm.cnt[1][b0] = sm.cnt[1][b1] = 0u;
     unsigned cur = 0xffffffffu, bkt_off = 0;
     CellParams<U> cp{};
     TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
@@ -68,6 +69,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     load_tile<K, IPT>(k, src_k, g);
     if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
     unsigned long long moved = 0;
+    __syncthreads();
     for (unsigned t = t0; t < t1; ++t) {
         const int p = (t - t0) & 1;
         TileGeo gn{};
@@ -86,44 +88,62 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
             cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m, sm.scan);  // syncs inside
         }
         const unsigned nb = 2 * cp.m + 1;
-        for (unsigned b = threadIdx.x; b < nb; b += kQsNT) sm.cnt[b] = 0;
-        __syncthreads();
+        unsigned* cnt = sm.cnt[p];
         moved += g.tn;
         // classify + rank: (bucket << 16) | rank within the tile
         unsigned br[IPT];
+        if (g.tn == TILE) {
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            const unsigned b = ct_classify(sm.ct, cp, OKey<K>::of(k[i]));
-            br[i] = (i * kQsNT + threadIdx.x < g.tn) ? ((b << 16) | atomicAdd(&sm.cnt[b], 1u)) : 0xffffffffu;
+            for (int i = 0; i < IPT; ++i) {
+                const unsigned b = ct_classify(sm.ct, cp, k[i]);
+                br[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                const unsigned b = ct_classify(sm.ct, cp, k[i]);
+                br[i] = (i * kQsNT + threadIdx.x < g.tn) ? ((b << 16) | atomicAdd(&cnt[b], 1u)) : 0xffffffffu;
+            }
         }
         __syncthreads();
-        // bucket offsets in the tile (2 buckets per thread) + run reservations
+        // bucket offsets in the tile (2 buckets per thread, in place) + run reservations
         typename ScatterPipeSmem<K, V>::Stage& S = sm.st[p];
-        const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;
-        const unsigned c0 = b0 < nb ? sm.cnt[b0] : 0u, c1 = b1 < nb ? sm.cnt[b1] : 0u;
+        const unsigned c0 = b0 < nb ? cnt[b0] : 0u, c1 = b1 < nb ? cnt[b1] : 0u;
         unsigned tot;
         const unsigned ex = block_excl_scan<kQsNT>(c0 + c1, sm.scan, &tot);
         unsigned long long r0 = 0, r1 = 0;
         if (c0) r0 = atomicAdd(&bkt_pool[bkt_off + b0], (unsigned long long)c0);
         if (c1) r1 = atomicAdd(&bkt_pool[bkt_off + b1], (unsigned long long)c1);
-        if (b0 < nb) S.loc[b0] = ex;
-        if (b1 < nb) S.loc[b1] = ex + c0;
+        if (b0 < nb) cnt[b0] = ex;
+        if (b1 < nb) cnt[b1] = ex + c0;
         if (threadIdx.x == 0) S.tn = g.tn;
         // overlap: write out the previous tile while the reservations fly
         if (t > t0) stage_writeout<K, V>(sm.st[p ^ 1], dst_k, dst_v);
-        if (c0) S.gbase[b0] = r0;
-        if (c1) S.gbase[b1] = r1;
-        __syncthreads();  // S.loc complete
+        if (c0) S.delta[b0] = r0 - ex;
+        if (c1) S.delta[b1] = r1 - (ex + c0);
+        __syncthreads();  // offsets complete; previous stage written out
+        unsigned* nxt = sm.cnt[p ^ 1];  // the previous tile's offsets are dead: clear for tile t+1
+        if (owner) nxt[b0] = nxt[b1] = 0u;
+        if (g.tn == TILE) {
 #pragma unroll
-        for (int i = 0; i < IPT; ++i) {
-            if (br[i] != 0xffffffffu) {
-                const unsigned slot = S.loc[br[i] >> 16] + (br[i] & 0xffffu);
+            for (int i = 0; i < IPT; ++i) {
+                const unsigned slot = cnt[br[i] >> 16] + (br[i] & 0xffffu);
                 S.k[slot] = k[i];
                 if constexpr (KV) S.v[slot] = v[i];
                 S.b[slot] = (unsigned short)(br[i] >> 16);
             }
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; ++i) {
+                if (br[i] != 0xffffffffu) {
+                    const unsigned slot = cnt[br[i] >> 16] + (br[i] & 0xffffu);
+                    S.k[slot] = k[i];
+                    if constexpr (KV) S.v[slot] = v[i];
+                    S.b[slot] = (unsigned short)(br[i] >> 16);
+                }
+            }
         }
-        __syncthreads();  // stage complete; previous stage free
+        __syncthreads();  // stage complete; counts for t+1 cleared
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             k[i] = kn[i];

@@ -92,6 +92,30 @@ __device__ __forceinline__ BulkTile issue_tile(char* buf, const T* src, uint64_t
     return bt;
 }
 
+// Window variant: when the 16-byte aligned window around the tile lies
+// inside the array [src, src + n_all), copy the whole window so that every
+// element of the tile is in shared memory (head = 0, body = tn); `buf` needs
+// tn*sizeof(T) + 32 bytes.  Otherwise fall back to issue_tile (interior only).
+template <typename T>
+__device__ __forceinline__ BulkTile issue_tile_window(char* buf, const T* src, uint64_t n_all, uint64_t base,
+                                                      unsigned tn, uint64_t* bar) {
+    const uintptr_t p0 = reinterpret_cast<uintptr_t>(src + base);
+    const uintptr_t p1 = reinterpret_cast<uintptr_t>(src + base + tn);
+    const uintptr_t a0 = p0 & ~(uintptr_t)15, a1 = (p1 + 15) & ~(uintptr_t)15;
+    if (tn == 0 || a0 < reinterpret_cast<uintptr_t>(src) || a1 > reinterpret_cast<uintptr_t>(src + n_all))
+        return issue_tile<T>(buf, src, base, tn, bar);
+    BulkTile bt;
+    bt.base = base;
+    bt.tn = tn;
+    bt.seg = 0;
+    bt.shift = (unsigned)(p0 - a0);
+    bt.head = 0;
+    bt.body = tn;
+    mbar_arrive_expect_tx(bar, (unsigned)(a1 - a0));
+    bulk_g2s(buf, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), bar);
+    return bt;
+}
+
 // Element i of a staged tile (after the stage's barrier phase completed).
 template <typename T>
 __device__ __forceinline__ T tile_get(const char* buf, const BulkTile& bt, const T* src, unsigned i) {

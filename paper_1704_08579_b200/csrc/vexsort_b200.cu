@@ -243,7 +243,8 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             VX_LAUNCHED();
             {
                 Launch l(KC_HIST, st);
-                qs_hist_kernel<K><<<g_hist, kQsNT, hist_smem_bytes<K>(), st>>>(src_k, segs[level & 1], c, towner, spl, bkt);
+                qs_hist_kernel<K><<<g_hist, kQsNT, hist_smem_bytes<K>(), st>>>(src_k, n, segs[level & 1], c, towner,
+                                                                                spl, bkt);
             }
             VX_LAUNCHED();
             {
