@@ -197,12 +197,14 @@ KERNEL_REGEX = {"qs_plan": "qs_plan_kernel", "qs_hist": "qs_hist_kernel", "qs_em
                 "bucket_partition": "bp_scatter_kernel"}
 
 
-def ncu_traffic(kernel_class):
-    """Per-launch DRAM bytes from the committed ncu --set full summary."""
+def ncu_traffic(workload, kernel_class):
+    """DRAM bytes per launch of `kernel_class` in one step of `workload`, from
+    the committed ncu --set full capture (tools/summarize_ncu.py), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(KERNEL_REGEX.get(kernel_class, kernel_class))
+        e = d.get(workload, {}).get(KERNEL_REGEX.get(kernel_class, kernel_class))
+        return None if e is None else round(e["bytes_per_launch"])
     except Exception:
         return None
 
@@ -309,7 +311,7 @@ def run_ours(args, spec, rank, world, local):
         alg_bytes = per_elem * n * args.steps + 8 * (len(offs)) * args.steps
     achieved = alg_bytes / (kms[dom] / 1e3) / 1e9 if kms[dom] > 0 else 0.0
     roof = {"bound": "hbm", "kernel": CLASSES[dom], "achieved": round(achieved, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(CLASSES[dom]),
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, CLASSES[dom]) if args.n is None else None,
             "peak_source": peak_src,
             "alg_bytes_per_launch": int(alg_bytes / max(launches[dom], 1)),
             "avg_launch_ms": round(kms[dom] / max(launches[dom], 1), 4)}

@@ -1,12 +1,16 @@
 """Summarise ncu evidence into profiles/.
 
-    python tools/summarize_ncu.py --full REP.ncu-rep [...] --launches LAUNCHES.csv --tag r1
+    python tools/summarize_ncu.py --full REP.ncu-rep[:WORKLOAD] [...] --launches LAUNCHES.csv --tag r1
 
 Writes profiles/ncu_summary_<tag>.md (per-launch duration, DRAM bytes, DRAM
 GB/s and % of the measured HBM peak, SM/L1 throughput, registers, occupancy)
-and profiles/ncu_traffic.json (per-kernel DRAM bytes per launch, read by
-bench.py as roofline.traffic), plus a share-of-step table from the
-gpu__time_duration launch list.
+and profiles/ncu_traffic.json, plus a share-of-step table from the
+gpu__time_duration launch list.  A report tagged with a bench workload is
+expected to hold every launch of ONE step of that workload (bench.py
+--steps 1 --warmup 0 under ncu); its per-kernel DRAM bytes averaged over the
+step's launches are stored under ncu_traffic.json[workload][kernel] and read
+by bench.py as roofline.traffic (comparable to alg_bytes_per_launch, which is
+averaged over the same launches).
 """
 
 import argparse
@@ -99,22 +103,28 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath))
+        traffic = {k: v for k, v in traffic.items() if isinstance(v, dict)}  # drop the old flat format
     if a.full:
         lines += ["## `ncu --set full --clock-control none` (cold, serialised launches)", "",
                   "| report | kernel | grid x block | regs | ms | DRAM read GB | DRAM write GB | DRAM GB/s | % of HBM peak "
                   "| mem-pipe % | SM % | L1 % | warps active % |",
                   "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
-        for rep in a.full:
+        for spec in a.full:
+            rep, _, wl = spec.partition(":")
+            acc = {}
             for r in full_rows(rep):
                 lines.append(f"| {r['report']} | `{r['kernel']}` | {r['grid']}x{r['block']} | {r['regs']} | "
                              f"{r['ms']:.3f} | {r['dram_read']/1e9:.3f} | {r['dram_write']/1e9:.3f} | "
                              f"{r['dram_gbs']:.0f} | {100*r['dram_gbs']/peak:.1f} | {r['mem_pct']:.1f} | "
                              f"{r['sm_pct']:.1f} | {r['l1_pct']:.1f} | {r['warps_active_pct']:.1f} |")
                 base = r["kernel"].split("<")[0]
-                cur = traffic.get(base)
-                tb = r["dram_read"] + r["dram_write"]
-                if cur is None or tb > cur:  # keep the biggest launch (the steady-state level)
-                    traffic[base] = tb
+                a_ = acc.setdefault(base, [0, 0.0, 0.0])
+                a_[0] += 1
+                a_[1] += r["dram_read"] + r["dram_write"]
+                a_[2] += r["ms"]
+            if wl:
+                traffic[wl] = {k: {"bytes_per_launch": v[1] / v[0], "launches": v[0], "ms_per_launch": v[2] / v[0]}
+                               for k, v in acc.items()}
         lines.append("")
     if a.launches:
         agg = launch_rows(a.launches)
