@@ -11,7 +11,7 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   > gpurun_out/prof/launches_default.log 2>&1
 echo "launch list rc=$?"
 for w in $WL; do
-  timeout 1500 ncu --set full --import-source on --clock-control none -k 'regex:^(qs_|partition2|segsort|bp_)' \
+  timeout 1500 ncu --set full --import-source on --clock-control none -k 'regex:(qs_|partition2|segsort|bp_)' \
     -o gpurun_out/prof/full_$w -f python bench.py --workload $w --steps 1 --warmup 0 --no-e2e --no-cpu \
     > gpurun_out/prof/full_$w.log 2>&1
   echo "full $w rc=$?"
