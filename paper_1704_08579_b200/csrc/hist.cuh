@@ -67,10 +67,10 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
 
     auto issue = [&](unsigned t, unsigned stage) {  // one thread
         const TileGeo g = tile_geo<TILE>(t, tile_owner, segs);
-        BulkTile bt = issue_tile_window<K>(reinterpret_cast<char*>(smem_raw) + stage * BUF, src, n_all, g.base,
-                                           g.tn, &s_full[stage]);
+        BulkTile bt = plan_tile<K>(src, n_all, g.base, g.tn);
         bt.seg = g.seg;
-        s_meta[stage] = bt;
+        s_meta[stage] = bt;  // before the arrive (release): consumers read it after their acquire
+        issue_planned(reinterpret_cast<char*>(smem_raw) + stage * BUF, bt, &s_full[stage]);
     };
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {

@@ -64,56 +64,64 @@ struct BulkTile {
     unsigned shift; // byte offset of element 0 inside the stage buffer
     unsigned head;  // elements before the bulk-copied interior
     unsigned body;  // elements in the bulk-copied interior
+    uintptr_t src;  // bulk copy: global source (16-byte aligned)
+    unsigned dst;   // bulk copy: byte offset in the stage buffer
+    unsigned bytes; // bulk copy: size (0: nothing to copy)
 };
 
-// Issue (one thread) the copy of elements [base, base+tn) of `src` into the
-// stage buffer `buf` (16-byte aligned, >= tn*sizeof(T) + 16 bytes) and arm
-// `bar` for it.  Returns the metadata consumers need.
+// Plan (no side effects) the copy of elements [base, base+tn) of `src` into
+// a stage buffer (16-byte aligned, >= tn*sizeof(T) + 32 bytes).  When the
+// 16-byte aligned window around the tile lies inside [src, src + n_all) the
+// whole window is copied, so every element of the tile is in shared memory
+// (head = 0, body = tn); otherwise only the aligned interior is.
 template <typename T>
-__device__ __forceinline__ BulkTile issue_tile(char* buf, const T* src, uint64_t base, unsigned tn, uint64_t* bar) {
+__device__ __forceinline__ BulkTile plan_tile(const T* src, uint64_t n_all, uint64_t base, unsigned tn) {
     BulkTile bt;
     bt.base = base;
     bt.tn = tn;
     bt.seg = 0;
     const uintptr_t p0 = reinterpret_cast<uintptr_t>(src + base);
     const uintptr_t p1 = reinterpret_cast<uintptr_t>(src + base + tn);
+    const uintptr_t w0 = p0 & ~(uintptr_t)15, w1 = (p1 + 15) & ~(uintptr_t)15;
+    if (tn > 0 && w0 >= reinterpret_cast<uintptr_t>(src) && w1 <= reinterpret_cast<uintptr_t>(src + n_all)) {
+        bt.shift = (unsigned)(p0 - w0);
+        bt.head = 0;
+        bt.body = tn;
+        bt.src = w0;
+        bt.dst = 0;
+        bt.bytes = (unsigned)(w1 - w0);
+        return bt;
+    }
     const uintptr_t a0 = (p0 + 15) & ~(uintptr_t)15, a1 = p1 & ~(uintptr_t)15;
     bt.shift = (unsigned)(p0 & 15);
     if (a1 > a0) {
         bt.head = (unsigned)((a0 - p0) / sizeof(T));
         bt.body = (unsigned)((a1 - a0) / sizeof(T));
-        mbar_arrive_expect_tx(bar, (unsigned)(a1 - a0));
-        bulk_g2s(buf + bt.shift + (a0 - p0), reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), bar);
+        bt.src = a0;
+        bt.dst = bt.shift + (unsigned)(a0 - p0);
+        bt.bytes = (unsigned)(a1 - a0);
     } else {
         bt.head = tn;  // nothing bulk-copied: every element comes from global
         bt.body = 0;
-        mbar_arrive(bar);
+        bt.src = 0;
+        bt.dst = 0;
+        bt.bytes = 0;
     }
     return bt;
 }
 
-// Window variant: when the 16-byte aligned window around the tile lies
-// inside the array [src, src + n_all), copy the whole window so that every
-// element of the tile is in shared memory (head = 0, body = tn); `buf` needs
-// tn*sizeof(T) + 32 bytes.  Otherwise fall back to issue_tile (interior only).
-template <typename T>
-__device__ __forceinline__ BulkTile issue_tile_window(char* buf, const T* src, uint64_t n_all, uint64_t base,
-                                                      unsigned tn, uint64_t* bar) {
-    const uintptr_t p0 = reinterpret_cast<uintptr_t>(src + base);
-    const uintptr_t p1 = reinterpret_cast<uintptr_t>(src + base + tn);
-    const uintptr_t a0 = p0 & ~(uintptr_t)15, a1 = (p1 + 15) & ~(uintptr_t)15;
-    if (tn == 0 || a0 < reinterpret_cast<uintptr_t>(src) || a1 > reinterpret_cast<uintptr_t>(src + n_all))
-        return issue_tile<T>(buf, src, base, tn, bar);
-    BulkTile bt;
-    bt.base = base;
-    bt.tn = tn;
-    bt.seg = 0;
-    bt.shift = (unsigned)(p0 - a0);
-    bt.head = 0;
-    bt.body = tn;
-    mbar_arrive_expect_tx(bar, (unsigned)(a1 - a0));
-    bulk_g2s(buf, reinterpret_cast<const void*>(a0), (unsigned)(a1 - a0), bar);
-    return bt;
+// Issue (one thread) a planned copy and arm `bar` for it.  Everything the
+// consumers read about the tile (its BulkTile, stored to shared memory) must
+// be written BEFORE this call: the arrive is a release and the consumers'
+// phase wait an acquire, which orders those stores.  (A copy of zero bytes
+// completes the phase at the arrive itself.)
+__device__ __forceinline__ void issue_planned(char* buf, const BulkTile& bt, uint64_t* bar) {
+    if (bt.bytes) {
+        mbar_arrive_expect_tx(bar, bt.bytes);
+        bulk_g2s(buf + bt.dst, reinterpret_cast<const void*>(bt.src), bt.bytes, bar);
+    } else {
+        mbar_arrive(bar);
+    }
 }
 
 // Element i of a staged tile (after the stage's barrier phase completed).
