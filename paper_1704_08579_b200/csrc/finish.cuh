@@ -43,6 +43,7 @@ constexpr int kFinMaxSample = 512;
 constexpr unsigned kWarpSortMax = 256;
 
 __device__ __forceinline__ unsigned pad32(unsigned i) { return i + (i >> 5); }
+__device__ __forceinline__ unsigned wmax_of(unsigned leaf) { return leaf < kWarpSortMax ? leaf : kWarpSortMax; }
 
 template <typename K, typename V>
 struct FinSmem {
@@ -61,7 +62,35 @@ struct FinSmem {
     unsigned short nxt[kFinMaxBkt + 1];  // greedy group successor of each bucket
     unsigned short grp[kFinMaxBkt + 2];  // group boundaries (bucket ids)
     unsigned scan[kFinNT / 32 + 1];
+    U rmin[kFinNT / 32], rmax[kFinNT / 32];  // per-warp key-code range
 };
+
+template <typename U>
+__device__ __forceinline__ U warp_min_u(U v) {
+    if constexpr (sizeof(U) == 4) {
+        return __reduce_min_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const U o = __shfl_xor_sync(0xffffffffu, v, d);
+            v = o < v ? o : v;
+        }
+        return v;
+    }
+}
+template <typename U>
+__device__ __forceinline__ U warp_max_u(U v) {
+    if constexpr (sizeof(U) == 4) {
+        return __reduce_max_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const U o = __shfl_xor_sync(0xffffffffu, v, d);
+            v = o > v ? o : v;
+        }
+        return v;
+    }
+}
 
 // Sort P = 32*E padded-smem slots b[pad32(lo + q)], q < c, in place with one
 // warp (blocked layout, sentinel padding by count).
@@ -161,6 +190,90 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
             if constexpr (KV) y[j] = ld_stream(src_v + start + p);
         }
     }
+    // 2. interpolation buckets: nbl equal-width key-code intervals over the
+    //    range's own [min, max] -- evenly spaced pivots, no sample.  Taken
+    //    whenever every bucket fits one warp network; otherwise (skewed or
+    //    clustered keys) the sampled pivots below decide.
+    bool linear = false;
+    unsigned nb = 0, m = 0;
+    unsigned br[IPT];
+#ifndef VX_FIN_LTARGET4
+#define VX_FIN_LTARGET4 100
+#endif
+#ifndef VX_FIN_LTARGET8
+#define VX_FIN_LTARGET8 40
+#endif
+    {
+        constexpr unsigned kLTarget = kGroup ? VX_FIN_LTARGET8 : VX_FIN_LTARGET4;
+        U lo = ~(U)0, hi = 0;
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (j * kFinNT + tid < len) {
+                const U u = OKey<K>::of(x[j]);
+                lo = u < lo ? u : lo;
+                hi = u > hi ? u : hi;
+            }
+        }
+        lo = warp_min_u(lo);
+        hi = warp_max_u(hi);
+        if (lane == 0) {
+            sm.rmin[tid >> 5] = lo;
+            sm.rmax[tid >> 5] = hi;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int w = 0; w < kFinNT / 32; ++w) {
+            lo = sm.rmin[w] < lo ? sm.rmin[w] : lo;
+            hi = sm.rmax[w] > hi ? sm.rmax[w] : hi;
+        }
+        if (lo == hi) {  // every key equal: the range is sorted as it stands
+            if (src_k != dst_k) {
+#pragma unroll
+                for (int j = 0; j < IPT; ++j) {
+                    const unsigned p = j * kFinNT + tid;
+                    if (p < len) {
+                        dst_k[start + p] = x[j];
+                        if constexpr (KV) dst_v[start + p] = y[j];
+                    }
+                }
+            }
+            __syncthreads();
+            return;
+        }
+        const unsigned ltarget = max(2u, min(kLTarget, leaf * 7 / 16));
+        unsigned nbl = min((unsigned)kFinMaxBkt, max(1u, (len + ltarget - 1) / ltarget));
+        const U range = hi - lo;
+        const unsigned bits = (unsigned)(8 * sizeof(U)) -
+                              (sizeof(U) == 8 ? (unsigned)__clzll((long long)range) : (unsigned)__clz((int)range));
+        const unsigned sh = bits > 32 ? bits - 32 : 0u;
+        const uint32_t r32 = (uint32_t)(range >> sh);
+        // bucket = floor(d * nbl / (r32 + 1)) as a high multiply; a range
+        // narrower than nbl gets one bucket per value
+        uint32_t mul;
+        if ((uint64_t)r32 + 1 <= nbl) {
+            nbl = r32 + 1;
+            mul = 0;
+        } else {
+            mul = (uint32_t)(((uint64_t)nbl << 32) / ((uint64_t)r32 + 1));
+        }
+        if (tid < nbl) sm.cnt[tid] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < IPT; ++j) {
+            if (j * kFinNT + tid < len) {
+                const uint32_t d = (uint32_t)((OKey<K>::of(x[j]) - lo) >> sh);
+                const unsigned b = mul ? __umulhi(d, mul) : d;
+                br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
+            }
+        }
+        __syncthreads();
+        const bool over = __syncthreads_or(tid < nbl && sm.cnt[tid] > wmax_of(leaf));
+        if (!over) {
+            linear = true;
+            nb = nbl;
+        }
+    }
+    if (!linear) {
     if (tid < S) {
         const uint64_t h = mix64(seed ^ (start * 0x2545F4914F6CDD1DULL + tid));
         if (len >= 2 * kFinNT) {
@@ -214,19 +327,13 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         cand = samp[q];
         keep = tid == 0 ? 1u : (samp[(unsigned)(((uint64_t)tid * S) / (mt + 1))] < cand ? 1u : 0u);
     }
-    unsigned m;
     const unsigned rank = block_excl_scan<kFinNT>(keep, sm.scan, &m);
-    const unsigned nb = 2 * m + 1;
+    nb = 2 * m + 1;
     if (keep) sm.ct.spl[rank] = cand;
     if (tid < nb) sm.cnt[tid] = 0;
-    if (tid == 0) {
-        sm.next_bucket = 0;
-        sm.grp[0] = 0;
-    }
     __syncthreads();
     const CellParams<U> cp = ct_build<kFinNT, false>(sm.ct, m, sm.scan);  // code map (narrow ranges); ends with a barrier
     // 4. classify once, rank with smem atomics (bucket << 16 | rank)
-    unsigned br[IPT];
 #pragma unroll
     for (int j = 0; j < IPT; ++j) {
         const unsigned p = j * kFinNT + tid;
@@ -234,6 +341,11 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
             const unsigned b = ct_classify(sm.ct, cp, x[j]);
             br[j] = (b << 16) | atomicAdd(&sm.cnt[b], 1u);
         }
+    }
+    }  // sampled pivots
+    if (tid == 0) {
+        sm.next_bucket = 0;
+        sm.grp[0] = 0;
     }
     __syncthreads();
     {
@@ -261,7 +373,7 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     //    above the leaf bound -- re-queued (written out unsorted below);
     //    an equal-to-pivot bucket alone is final.
     const unsigned wmax = min(leaf, kWarpSortMax);
-    unsigned ngrp = m + 1;  // without grouping: the m+1 range buckets, one by one
+    unsigned ngrp = linear ? nb : m + 1;  // without grouping: the range buckets, one by one
     if constexpr (kGroup) {
         const unsigned G = min(wmax, kFinGroup);
         for (unsigned s = tid; s < nb; s += kFinNT) {
@@ -291,9 +403,9 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         if (lane == 0) j = atomicAdd(&sm.next_bucket, 1u);
         j = __shfl_sync(0xffffffffu, j, 0);
         if (j >= ngrp) break;
-        const unsigned s = kGroup ? sm.grp[j] : 2 * j, e = kGroup ? sm.grp[j + 1] : 2 * j + 1;
+        const unsigned s = kGroup ? sm.grp[j] : (linear ? j : 2 * j), e = kGroup ? sm.grp[j + 1] : s + 1;
         const unsigned lo = sm.loc[s], c = sm.loc[e] - lo;
-        if (c < 2 || (e == s + 1 && (s & 1u))) continue;  // trivial, or one equal-to-pivot bucket
+        if (c < 2 || (!linear && e == s + 1 && (s & 1u))) continue;  // trivial, or one equal-to-pivot bucket
         if (c <= wmax) {
             if constexpr (KV) warp_sort_smem<K, V>(sm.b, sm.bv, lo, c);
             else warp_sort_smem<K, V>(sm.b, (V*)nullptr, lo, c);
