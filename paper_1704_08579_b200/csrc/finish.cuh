@@ -198,7 +198,7 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     unsigned nb = 0, m = 0;
     unsigned br[IPT];
 #ifndef VX_FIN_LTARGET4
-#define VX_FIN_LTARGET4 100
+#define VX_FIN_LTARGET4 120
 #endif
 #ifndef VX_FIN_LTARGET8
 #define VX_FIN_LTARGET8 40
