@@ -10,7 +10,9 @@
 // so every element is read from shared memory with no edge tests.  Each
 // element is classified into one of 2m+1 buckets (ranges and equal-to-pivot
 // buckets) and counted in a shared histogram that is flushed to the
-// segment's global histogram once per (CTA, segment).
+// segment's global histogram once per (CTA, segment).  The bucket id of every
+// element is stored (u16, coalesced) for the scatter pass, which then ranks
+// and moves elements without classifying them again.
 #pragma once
 
 #include "common.cuh"
@@ -46,7 +48,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                                                         const Ctl* __restrict__ ctl,
                                                         const unsigned* __restrict__ tile_owner,
                                                         const K* __restrict__ spl_pool,
-                                                        unsigned long long* __restrict__ bkt_pool) {
+                                                        unsigned long long* __restrict__ bkt_pool,
+                                                        unsigned short* __restrict__ ids) {
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     constexpr unsigned BUF = (hist_stage_bytes<K>() + 127) / 128 * 128;
     constexpr int NS = hist_stages<K>();
@@ -111,15 +114,20 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
         if (bt.body == TILE) {  // the whole (full) tile is in shared memory
             const K* sb = reinterpret_cast<const K*>(buf + bt.shift);
 #pragma unroll
-            for (int i = 0; i < IPT; ++i)
-                atomicAdd(&s_hist[ct_classify(s_ct, cp, sb[i * kQsNT + tid])], 1u);
+            for (int i = 0; i < IPT; ++i) {
+                const unsigned b = ct_classify(s_ct, cp, sb[i * kQsNT + tid]);
+                atomicAdd(&s_hist[b], 1u);
+                ids[bt.base + i * kQsNT + tid] = (unsigned short)b;
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 const unsigned idx = i * kQsNT + tid;
                 if (idx < bt.tn) {
                     const K x = tile_get<K>(buf, bt, src, idx);
-                    atomicAdd(&s_hist[ct_classify(s_ct, cp, x)], 1u);
+                    const unsigned b = ct_classify(s_ct, cp, x);
+                    atomicAdd(&s_hist[b], 1u);
+                    ids[bt.base + idx] = (unsigned short)b;
                 }
             }
         }

@@ -1,7 +1,7 @@
 // scatter.cuh -- the partition level's scatter pass, software-pipelined.
 //
-// Per 4096-element tile: classify every element against the segment's
-// pivots (cell-table classifier), rank it inside its bucket with a shared
+// Per 4096-element tile: take every element's bucket (the id the histogram
+// pass stored while classifying it), rank it inside its bucket with a shared
 // memory atomic, reserve one run per non-empty bucket in the destination
 // with a global atomic, stage the tile bucket-major in shared memory and
 // write the runs with consecutive threads (coalesced).  The reservation is
@@ -28,7 +28,6 @@ struct ScatterPipeSmem {
     };
     Stage st[2];
     unsigned cnt[2][kMaxBkt + 1];  // per-tile counts, then (in place) bucket offsets; double-buffered
-    CellTable<typename OKey<K>::U> ct;
     unsigned scan[kQsNT / 32 + 1];
 };
 
@@ -44,14 +43,13 @@ __device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K,
 
 template <typename K, typename V>
 __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
+                                                           const unsigned short* __restrict__ ids,
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v,
                                                            const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
                                                            const unsigned* __restrict__ tile_owner,
-                                                           const K* __restrict__ spl_pool,
                                                            unsigned long long* __restrict__ bkt_pool) {
     constexpr bool KV = HasVal<V>::value;
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
-    using U = typename OKey<K>::U;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterPipeSmem<K, V>& sm = *reinterpret_cast<ScatterPipeSmem<K, V>*>(smem_raw);
     const unsigned ntiles = ctl->tile_ctr;
@@ -61,12 +59,13 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;  // the two buckets this thread scans / reserves
     const bool owner = b1 <= (unsigned)kMaxBkt;        // threads past the bucket range own none
     if (owner) sm.cnt[0][b0] = sm.cnt[0][b1] = sm.cnt[1][b0] = sm.cnt[1][b1] = 0u;
-    unsigned cur = 0xffffffffu, bkt_off = 0;
-    CellParams<U> cp{};
+    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0;
     TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
     K k[IPT];
     V v[IPT];
+    unsigned short id[IPT];
     load_tile<K, IPT>(k, src_k, g);
+    load_tile<unsigned short, IPT>(id, ids, g);
     if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
     unsigned long long moved = 0;
     __syncthreads();
@@ -75,33 +74,32 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         TileGeo gn{};
         K kn[IPT];
         V vn[IPT];
+        unsigned short idn[IPT];
         if (t + 1 < t1) {
             gn = tile_geo<TILE>(t + 1, tile_owner, segs);
             load_tile<K, IPT>(kn, src_k, gn);
+            load_tile<unsigned short, IPT>(idn, ids, gn);
             if constexpr (KV) load_tile<V, IPT>(vn, src_v, gn);
         }
         if (g.seg != cur) {
-            __syncthreads();
             cur = g.seg;
-            const Seg sg = segs[g.seg];
-            bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(sm.ct, spl_pool, sg.spl_off, sg.m, sm.scan);  // syncs inside
+            bkt_off = segs[g.seg].bkt_off;
+            nb = 2 * segs[g.seg].m + 1;
         }
-        const unsigned nb = 2 * cp.m + 1;
         unsigned* cnt = sm.cnt[p];
         moved += g.tn;
-        // classify + rank: (bucket << 16) | rank within the tile
+        // rank by the bucket id the histogram pass stored: (bucket << 16) | rank within the tile
         unsigned br[IPT];
         if (g.tn == TILE) {
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-                const unsigned b = ct_classify(sm.ct, cp, k[i]);
+                const unsigned b = id[i];
                 br[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
             }
         } else {
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-                const unsigned b = ct_classify(sm.ct, cp, k[i]);
+                const unsigned b = id[i];
                 br[i] = (i * kQsNT + threadIdx.x < g.tn) ? ((b << 16) | atomicAdd(&cnt[b], 1u)) : 0xffffffffu;
             }
         }
@@ -147,6 +145,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
 #pragma unroll
         for (int i = 0; i < IPT; ++i) {
             k[i] = kn[i];
+            id[i] = idn[i];
             if constexpr (KV) v[i] = vn[i];
         }
         g = gn;

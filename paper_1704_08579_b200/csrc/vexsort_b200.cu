@@ -72,7 +72,7 @@ struct SortLayout {
     uint64_t n = 0;
     uint64_t cap_seg = 0, cap_spl = 0, cap_bkt = 0, cap_tiles = 0, cap_fin = 0;
     size_t off_sk = 0, off_sv = 0, off_seg0 = 0, off_seg1 = 0, off_ctl = 0, off_spl = 0, off_bkt = 0,
-           off_tile = 0, off_fin = 0, total = 0;
+           off_tile = 0, off_fin = 0, off_ids = 0, total = 0;
 
     explicit SortLayout(uint64_t n_) : n(n_) {
         constexpr bool KV = HasVal<V>::value;
@@ -91,6 +91,7 @@ struct SortLayout {
         off_bkt = o; o = align_up(o + cap_bkt * sizeof(unsigned long long));
         off_tile = o; o = align_up(o + cap_tiles * sizeof(unsigned));
         off_fin = o; o = align_up(o + 2 * cap_fin * sizeof(Fin));  // ping-pong by level parity
+        off_ids = o; o = align_up(o + n * sizeof(unsigned short));  // per-element bucket ids (hist -> scatter)
         total = o;
     }
 };
@@ -194,6 +195,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     unsigned long long* bkt = reinterpret_cast<unsigned long long*>(w + lay.off_bkt);
     unsigned* towner = reinterpret_cast<unsigned*>(w + lay.off_tile);
     Fin* fins[2] = {reinterpret_cast<Fin*>(w + lay.off_fin), reinterpret_cast<Fin*>(w + lay.off_fin) + lay.cap_fin};
+    unsigned short* ids = reinterpret_cast<unsigned short*>(w + lay.off_ids);
     if (!HasVal<V>::value) sv = nullptr;
     // the bitonic leaf bound: the reference's sort_bound when given, else
     // the widest warp network (512); see DESIGN.md
@@ -244,7 +246,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             {
                 Launch l(KC_HIST, st);
                 qs_hist_kernel<K><<<g_hist, kQsNT, hist_smem_bytes<K>(), st>>>(src_k, n, segs[level & 1], c, towner,
-                                                                                spl, bkt);
+                                                                                spl, bkt, ids);
             }
             VX_LAUNCHED();
             {
@@ -258,7 +260,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             {
                 Launch l(KC_SCATTER, st);
                 qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterPipeSmem<K, V>), st>>>(
-                    src_k, src_v, dst_k, dst_v, segs[level & 1], c, towner, spl, bkt);
+                    src_k, src_v, ids, dst_k, dst_v, segs[level & 1], c, towner, bkt);
             }
             VX_LAUNCHED();
         }
