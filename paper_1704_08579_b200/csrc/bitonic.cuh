@@ -36,9 +36,14 @@ __device__ __forceinline__ uint32_t kmax(uint32_t a, uint32_t b) { return max(a,
 __device__ __forceinline__ uint64_t kmin(uint64_t a, uint64_t b) { return a < b ? a : b; }
 __device__ __forceinline__ uint64_t kmax(uint64_t a, uint64_t b) { return a < b ? b : a; }
 
-template <typename K, typename V, int E>
+// G (a power of two <= 32) lanes sort one network of P = G*E slots; a warp
+// runs 32/G independent networks side by side (every shuffle stays inside
+// its group of G lanes).  Fewer lanes and more registers per lane turn
+// cross-lane rounds (shuffle + two selects per slot) into in-register
+// rounds (one min/max per slot).
+template <typename K, typename V, int E, int G = 32>
 struct WarpBitonic {
-    static constexpr int P = 32 * E;
+    static constexpr int P = G * E;
     static constexpr bool KV = HasVal<V>::value;
 
     // one comparator round with XOR distance MASK over all P slots
@@ -69,25 +74,36 @@ struct WarpBitonic {
             constexpr int HB = 1 << (31 - __builtin_clz(LM));  // highest lane bit
             const int lane = threadIdx.x & 31;
             const bool low = (lane & HB) == 0;  // this lane holds the lower slots
-            // gather every partner value first (old values), then update
-            K pk[E];
-            V pv[E];
-#pragma unroll
-            for (int r = 0; r < E; ++r) {
-                pk[r] = __shfl_xor_sync(0xffffffffu, k[r ^ RM], LM);
-                if constexpr (KV) pv[r] = __shfl_xor_sync(0xffffffffu, v[r ^ RM], LM);
-            }
-#pragma unroll
-            for (int r = 0; r < E; ++r) {
+            // slot r's partner value is the partner lane's register r ^ RM;
+            // registers are updated pairwise {r, r ^ RM} from old values, so
+            // at most two partner values are live at a time
+            auto upd = [&](K& mk, V& mv, K pk, V pv) {
                 if constexpr (KV) {
                     // low side takes the partner iff partner < mine, high side
                     // iff partner > mine: strict inversion, branch-free
-                    const int lt = pk[r] < k[r], ne = pk[r] != k[r];
+                    const int lt = pk < mk, ne = pk != mk;
                     const int t = ne & (lt ^ (int)!low);
-                    k[r] = t ? pk[r] : k[r];
-                    v[r] = t ? pv[r] : v[r];
+                    mk = t ? pk : mk;
+                    mv = t ? pv : mv;
                 } else {
-                    k[r] = low ? kmin(k[r], pk[r]) : kmax(k[r], pk[r]);
+                    mk = low ? kmin(mk, pk) : kmax(mk, pk);
+                }
+            };
+#pragma unroll
+            for (int r = 0; r < E; ++r) {
+                const int r2 = r ^ RM;
+                if (r2 < r) continue;  // handled with its pair
+                const K pa = __shfl_xor_sync(0xffffffffu, k[r2], LM);
+                V va{};
+                if constexpr (KV) va = __shfl_xor_sync(0xffffffffu, v[r2], LM);
+                if (r2 == r) {
+                    upd(k[r], v[r], pa, va);
+                } else {
+                    const K pb = __shfl_xor_sync(0xffffffffu, k[r], LM);
+                    V vb{};
+                    if constexpr (KV) vb = __shfl_xor_sync(0xffffffffu, v[r], LM);
+                    upd(k[r], v[r], pa, va);
+                    upd(k[r2], v[r2], pb, vb);
                 }
             }
         }

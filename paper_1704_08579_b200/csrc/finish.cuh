@@ -56,7 +56,7 @@ struct FinSmem {
     U samp[kFinMaxSample];
     U samp2[kFinMaxSample];
     CellTableT<U, kFinMaxSplit + 1, kFinLutBits> ct;  // pivots + 1024-cell lookup table
-    unsigned next_bucket, ngrp;
+    unsigned next_bucket, next_big, ngrp;
     unsigned cnt[kFinMaxBkt + 1];
     unsigned loc[kFinMaxBkt + 2];
     unsigned short nxt[kFinMaxBkt + 1];  // greedy group successor of each bucket
@@ -119,6 +119,52 @@ __device__ __forceinline__ void warp_sort_smem_e(K* b, V* bv, unsigned lo, unsig
     }
     __syncwarp();
 }
+
+// Lane-group variant: every group of G lanes sorts its own run b[pad32(lo +
+// q)], q < c <= G*E (lo, c uniform within the group; c = 0 sorts padding
+// only and writes nothing).
+template <typename K, typename V, int E, int G>
+__device__ __forceinline__ void group_sort_smem(K* b, V* bv, unsigned lo, unsigned c) {
+    constexpr bool KV = HasVal<V>::value;
+    using R = KeyRep<K>;
+    using I = typename R::I;
+    const unsigned gl = threadIdx.x & (G - 1);
+    I k[E];
+    V v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const unsigned q = gl * E + r;
+        k[r] = q < c ? R::to(b[pad32(lo + q)]) : KeyTraits<I>::sentinel();
+        if constexpr (KV) v[r] = q < c ? bv[pad32(lo + q)] : V();
+    }
+    WarpBitonic<I, V, E, G>::sort(k, v);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const unsigned q = gl * E + r;
+        if (q < c) {
+            b[pad32(lo + q)] = R::from(k[r]);
+            if constexpr (KV) bv[pad32(lo + q)] = v[r];
+        }
+    }
+    __syncwarp();
+}
+
+// Group shape of the finish networks: 128 slots per group of G lanes -- 16
+// lanes x 8 registers for 8-byte keys and pairs; 4-byte keys use whole-warp
+// networks (G = 32: measured faster on B200 than 8 x 16 or 16 x 8 groups).
+template <typename K, typename V>
+struct FinGroupShape {
+    static constexpr int BYTES = sizeof(K) + (HasVal<V>::value ? sizeof(V) : 0);
+#ifndef VX_FIN_GLANES4
+#define VX_FIN_GLANES4 32
+#endif
+#ifndef VX_FIN_GLANES8
+#define VX_FIN_GLANES8 16
+#endif
+    static constexpr int G = BYTES <= 4 ? VX_FIN_GLANES4 : VX_FIN_GLANES8;
+    static constexpr int E = 128 / G;
+    static constexpr unsigned P = 128;
+};
 
 template <typename K, typename V>
 __device__ __forceinline__ void warp_sort_smem(K* b, V* bv, unsigned lo, unsigned c) {
@@ -345,6 +391,7 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
     }  // sampled pivots
     if (tid == 0) {
         sm.next_bucket = 0;
+        sm.next_big = 0;
         sm.grp[0] = 0;
     }
     __syncthreads();
@@ -398,14 +445,38 @@ __device__ void fin_local(FinSmem<K, V>& sm, const K* __restrict__ src_k, const 
         __syncthreads();
         ngrp = sm.ngrp;
     }
+    // 7a. runs of <= 128 slots: lane groups, 32/G runs per warp at a time
+    //     (measured: 16-lane groups win for 8-byte keys and pairs; 4-byte
+    //     keys keep one run per warp, 7b only)
+    using GS = FinGroupShape<K, V>;
+    constexpr unsigned NGW = 32 / GS::G;
+    const unsigned gmax = GS::G == 32 ? 0u : min(wmax, GS::P);
+    if constexpr (GS::G < 32) for (;;) {
+        unsigned j0 = 0;
+        if (lane == 0) j0 = atomicAdd(&sm.next_bucket, NGW);
+        j0 = __shfl_sync(0xffffffffu, j0, 0);
+        if (j0 >= ngrp) break;
+        const unsigned j = j0 + lane / GS::G;
+        unsigned lo = 0, c = 0;
+        if (j < ngrp) {
+            const unsigned s = kGroup ? sm.grp[j] : (linear ? j : 2 * j), e = kGroup ? sm.grp[j + 1] : s + 1;
+            lo = sm.loc[s];
+            c = sm.loc[e] - lo;
+            if (c < 2 || c > gmax || (!linear && e == s + 1 && (s & 1u))) c = 0;  // none, too big, or final
+        }
+        if constexpr (KV) group_sort_smem<K, V, GS::E, GS::G>(sm.b, sm.bv, lo, c);
+        else group_sort_smem<K, V, GS::E, GS::G>(sm.b, (V*)nullptr, lo, c);
+    }
+    // 7b. the rest (128 < c <= leaf bound) with whole-warp networks; above
+    //     the leaf bound re-queued
     for (;;) {
         unsigned j = 0;
-        if (lane == 0) j = atomicAdd(&sm.next_bucket, 1u);
+        if (lane == 0) j = atomicAdd(&sm.next_big, 1u);
         j = __shfl_sync(0xffffffffu, j, 0);
         if (j >= ngrp) break;
         const unsigned s = kGroup ? sm.grp[j] : (linear ? j : 2 * j), e = kGroup ? sm.grp[j + 1] : s + 1;
         const unsigned lo = sm.loc[s], c = sm.loc[e] - lo;
-        if (c < 2 || (!linear && e == s + 1 && (s & 1u))) continue;  // trivial, or one equal-to-pivot bucket
+        if (c <= gmax || (!linear && e == s + 1 && (s & 1u))) continue;  // done above, or one equal-to-pivot bucket
         if (c <= wmax) {
             if constexpr (KV) warp_sort_smem<K, V>(sm.b, sm.bv, lo, c);
             else warp_sort_smem<K, V>(sm.b, (V*)nullptr, lo, c);
