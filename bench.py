@@ -182,7 +182,7 @@ def gen(L, dtype_code, dist_code, t, seed, gofs, gn):
 
 
 def prof_read(L):
-    n = 8
+    n = 9
     la = (ctypes.c_int64 * n)()
     ms = (ctypes.c_double * n)()
     el = (ctypes.c_uint64 * n)()
@@ -190,11 +190,12 @@ def prof_read(L):
     return list(la), list(ms), list(el)
 
 
-CLASSES = ["qs_plan", "qs_hist", "qs_emit", "qs_scatter", "qs_finish", "partition2", "segsort", "bucket_partition"]
+CLASSES = ["qs_plan", "qs_hist", "qs_emit", "qs_scatter", "qs_finish", "partition2", "segsort", "bucket_partition",
+           "qs_local"]
 KERNEL_REGEX = {"qs_plan": "qs_plan_kernel", "qs_hist": "qs_hist_kernel", "qs_emit": "qs_emit_kernel",
                 "qs_scatter": "qs_scatter_kernel", "qs_finish": "qs_finish_kernel",
                 "partition2": "partition2_kernel", "segsort": "segsort_kernel",
-                "bucket_partition": "bp_scatter_kernel"}
+                "bucket_partition": "bp_scatter_kernel", "qs_local": "qs_local_kernel"}
 
 
 def ncu_traffic(workload, kernel_class):

@@ -71,6 +71,9 @@ struct Seg {
     unsigned long long start, len;
     unsigned spl_off, m, bkt_off, tile_base;
 };
+struct QlItemT {  // a segment for the CTA-local level (local.cuh)
+    unsigned long long start, len;
+};
 struct Fin {
     unsigned long long start;
     unsigned len, flags;  // bit0: source is the scratch buffer; bit1: copy only
@@ -81,6 +84,9 @@ struct Ctl {
     unsigned err;
     unsigned long long scat_elems;  // elements moved by this level's scatter
     unsigned long long fin_elems;   // elements finished (sorted / copied) at this level
+    unsigned long long loc_elems;   // elements sorted by the CTA-local level (local.cuh)
+    unsigned ql_ctr;                // CTA-local segments queued by this level's emit
+    unsigned pad_;
 };
 enum : unsigned { kErrCapacity = 1, kErrTooLong = 2 };
 
@@ -347,7 +353,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                                                           Ctl* __restrict__ ctl, K* __restrict__ spl_pool,
                                                           unsigned long long* __restrict__ bkt_pool,
                                                           unsigned* __restrict__ tile_owner, unsigned cap_spl,
-                                                          unsigned cap_bkt, unsigned cap_tiles, uint64_t seed) {
+                                                          unsigned cap_bkt, unsigned cap_tiles, uint64_t seed,
+                                                          uint64_t ql_target) {
     constexpr int TILE = qs_tile<K>();
     __shared__ K s_samp[kMaxSample];
     __shared__ unsigned s_scan[kPlanNT / 32 + 1];
@@ -355,9 +362,20 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
     const unsigned nseg = ctl->nseg;
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const uint64_t start = segs[s].start, len = segs[s].len;
-        // aim global-level buckets at half the CTA-local capacity
-        const uint64_t mt64 = len / (FinCap<K, V>::value / 2);
-        const unsigned mt = (unsigned)max((uint64_t)2, min((uint64_t)kMaxSplit, mt64));
+        unsigned mt;
+        if (ql_target == 0 || len <= 3 * ql_target) {
+            // aim the buckets at half the finish capacity
+            const uint64_t mt64 = len / (FinCap<K, V>::value / 2);
+            mt = (unsigned)max((uint64_t)2, min((uint64_t)kMaxSplit, mt64));
+        } else {
+            // aim the leaves of the remaining levels at the CTA-local level's
+            // target, fan-out balanced over them: L = ceil(log_256(r)) levels
+            // of r^(1/L) buckets, r = len / target
+            const double r = (double)len / (double)ql_target;
+            const double L = ceil(log(r) / log(256.0) - 1e-9);
+            const double f = ceil(pow(r, 1.0 / (L < 1.0 ? 1.0 : L)) - 1e-9);
+            mt = (unsigned)max(2.0, min((double)kMaxSplit, f - 1.0));
+        }
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
         for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
@@ -468,7 +486,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                                                           Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
                                                           unsigned long long* __restrict__ bkt_pool,
                                                           Fin* __restrict__ fins, unsigned cap_seg, unsigned cap_fin,
-                                                          int dst_is_scratch) {
+                                                          int dst_is_scratch, QlItemT* __restrict__ qls,
+                                                          uint64_t ql_cap) {
     static_assert(kPlanNT >= kMaxBkt, "one thread per bucket");
     constexpr uint32_t LOCAL = FinCap<K, V>::value;
     __shared__ unsigned long long s_scan[kPlanNT / 32];
@@ -507,6 +526,14 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                         fins[f].start = bstart;
                         fins[f].len = (unsigned)c;
                         fins[f].flags = dst_is_scratch ? 1u : 0u;
+                    }
+                } else if (c <= ql_cap) {
+                    unsigned q = atomicAdd(&ctl->ql_ctr, 1u);
+                    if (q >= cap_seg) {
+                        atomicOr(&ctl->err, kErrCapacity);
+                    } else {
+                        qls[q].start = bstart;
+                        qls[q].len = c;
                     }
                 } else {
                     unsigned q = atomicAdd(&ctl_next->nseg, 1u);

@@ -17,6 +17,7 @@
 #include "finish.cuh"
 #include "scatter.cuh"
 #include "hist.cuh"
+#include "local.cuh"
 
 using namespace vx;
 
@@ -72,7 +73,7 @@ struct SortLayout {
     uint64_t n = 0;
     uint64_t cap_seg = 0, cap_spl = 0, cap_bkt = 0, cap_tiles = 0, cap_fin = 0;
     size_t off_sk = 0, off_sv = 0, off_seg0 = 0, off_seg1 = 0, off_ctl = 0, off_spl = 0, off_bkt = 0,
-           off_tile = 0, off_fin = 0, off_ids = 0, total = 0;
+           off_tile = 0, off_fin = 0, off_ids = 0, off_ql = 0, total = 0;
 
     explicit SortLayout(uint64_t n_) : n(n_) {
         constexpr bool KV = HasVal<V>::value;
@@ -92,6 +93,7 @@ struct SortLayout {
         off_tile = o; o = align_up(o + cap_tiles * sizeof(unsigned));
         off_fin = o; o = align_up(o + 2 * cap_fin * sizeof(Fin));  // ping-pong by level parity
         off_ids = o; o = align_up(o + n * sizeof(unsigned short));  // per-element bucket ids (hist -> scatter)
+        off_ql = o; o = align_up(o + cap_seg * sizeof(QlItemT));      // CTA-local level queue
         total = o;
     }
 };
@@ -108,7 +110,8 @@ thread_local PinnedScratch g_pinned;
 // ----------------------------------------------------------- instrumentation
 // Launch counting is always on; per-launch CUDA-event timing is opt-in
 // (vx_profile_enable) and brackets each kernel on its own stream.
-enum KClass { KC_PLAN = 0, KC_HIST, KC_EMIT, KC_SCATTER, KC_FINISH, KC_PARTITION, KC_SEGSORT, KC_BUCKET, KC_N };
+enum KClass { KC_PLAN = 0, KC_HIST, KC_EMIT, KC_SCATTER, KC_FINISH, KC_PARTITION, KC_SEGSORT, KC_BUCKET, KC_LOCAL,
+              KC_N };
 struct KProf {
     std::mutex mu;
     bool on = false;
@@ -196,15 +199,24 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     unsigned* towner = reinterpret_cast<unsigned*>(w + lay.off_tile);
     Fin* fins[2] = {reinterpret_cast<Fin*>(w + lay.off_fin), reinterpret_cast<Fin*>(w + lay.off_fin) + lay.cap_fin};
     unsigned short* ids = reinterpret_cast<unsigned short*>(w + lay.off_ids);
-    if (!HasVal<V>::value) sv = nullptr;
     // the bitonic leaf bound: the reference's sort_bound when given, else
     // the widest warp network (512); see DESIGN.md
     const unsigned leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
+    QlItemT* qls = reinterpret_cast<QlItemT*>(w + lay.off_ql);
+#ifndef VX_NO_QL
+    // the CTA-local level needs leaves of ~2x its bucket target (skipped for a small sort_bound)
+    const bool ql_on = leaf >= 2 * QlCfg<K, V>::LT;
+#else
+    const bool ql_on = false;
+#endif
+    const uint64_t ql_target = ql_on ? QlCfg<K, V>::TARGET : 0, ql_cap = ql_on ? QlCfg<K, V>::CAP : 0;
+    if (!HasVal<V>::value) sv = nullptr;
 
     const int sms = num_sms();
     static int occ_hist = prepare(qs_hist_kernel<K>, kQsNT, hist_smem_bytes<K>());
     static int occ_scat = prepare(qs_scatter_kernel<K, V>, kQsNT, sizeof(ScatterPipeSmem<K, V>));
     static int occ_fin = prepare(qs_finish_kernel<K, V>, kFinNT, sizeof(FinSmem<K, V>));
+    static int occ_loc = prepare(qs_local_kernel<K, V>, kQlNT, sizeof(QlSmem<K, V>));
     const int g_hist = sms * occ_hist, g_scat = sms * occ_scat, g_fin = sms * occ_fin;
 
     VX_CUDA(cudaMemsetAsync(ctl, 0, kMaxLevels * sizeof(Ctl), st));
@@ -240,7 +252,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
                 Launch l(KC_PLAN, st);
                 qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, segs[level & 1], c, spl, bkt, towner,
                                                                  (unsigned)lay.cap_spl, (unsigned)lay.cap_bkt,
-                                                                 (unsigned)lay.cap_tiles, lvl_seed);
+                                                                 (unsigned)lay.cap_tiles, lvl_seed, ql_target);
             }
             VX_LAUNCHED();
             {
@@ -254,13 +266,21 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
                 qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
                                                                  segs[(level + 1) & 1], bkt, fins[level & 1],
                                                                  (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
-                                                                 even ? 1 : 0);
+                                                                 even ? 1 : 0, qls, ql_cap);
             }
             VX_LAUNCHED();
             {
                 Launch l(KC_SCATTER, st);
                 qs_scatter_kernel<K, V><<<g_scat, kQsNT, sizeof(ScatterPipeSmem<K, V>), st>>>(
                     src_k, src_v, ids, dst_k, dst_v, segs[level & 1], c, towner, bkt);
+            }
+            VX_LAUNCHED();
+            if (ql_cap) {
+                // medium children: CTA-local last level + leaves (data in dst, other buffer = src side)
+                Launch l(KC_LOCAL, st);
+                qs_local_kernel<K, V><<<sms * occ_loc, kQlNT, sizeof(QlSmem<K, V>), st>>>(
+                    qls, c, ctl + level + 1, segs[(level + 1) & 1], (unsigned)lay.cap_seg, dst_k, dst_v,
+                    even ? keys : sk, even ? vals : sv, keys, vals, leaf);
             }
             VX_LAUNCHED();
         }
@@ -276,17 +296,18 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         // next level's queue sizes, error flags and element counters -> host
         VX_CUDA(cudaMemcpyAsync(hp, &ctl[level + 1].nseg, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaMemcpyAsync(hp + 1, &c->err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaMemcpyAsync(hp + 2, &c->scat_elems, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaMemcpyAsync(hp + 4, &ctl[level + 1].fin_ctr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        VX_CUDA(cudaMemcpyAsync(hp + 2, &c->scat_elems, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        VX_CUDA(cudaMemcpyAsync(hp + 5, &ctl[level + 1].fin_ctr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaStreamSynchronize(st));
         if (g_prof.on) {
             prof_elems(KC_SCATTER, hp[2]);
             prof_elems(KC_FINISH, hp[3]);
+            prof_elems(KC_LOCAL, hp[4]);
             prof_collect();
         }
         if ((unsigned)hp[1]) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
         nseg = (unsigned)hp[0];
-        if (nseg == 0 && (unsigned)hp[4] == 0) return VX_OK;
+        if (nseg == 0 && (unsigned)hp[5] == 0) return VX_OK;
     }
     return fail(VX_ECAPACITY, "sort exceeded the maximum level count");
 }

@@ -580,14 +580,15 @@ def test_profile_counters_report_launches_and_elements():
     vx.sort(x)
     torch.cuda.synchronize()
     L.vx_profile_enable(0)
-    la = (ctypes.c_int64 * 8)()
-    ms = (ctypes.c_double * 8)()
-    el = (ctypes.c_uint64 * 8)()
-    assert L.vx_profile_read(la, ms, el, 8) == 8
-    assert la[3] >= 1 and la[4] >= 1  # scatter, finish
+    la = (ctypes.c_int64 * 9)()
+    ms = (ctypes.c_double * 9)()
+    el = (ctypes.c_uint64 * 9)()
+    assert L.vx_profile_read(la, ms, el, 9) == 9
+    assert la[3] >= 1 and la[4] >= 1 and la[8] >= 1  # scatter, finish, CTA-local level
     assert el[3] >= (1 << 22)  # the first level moves every element
-    assert el[4] >= (1 << 21)  # most elements end in a finish item
-    assert ms[4] > 0.0
+    assert el[4] + el[8] >= (1 << 22)  # every element ends in a finish item or a CTA-local segment
+    assert el[8] >= (1 << 21)  # uniform keys: most segments go through the CTA-local level
+    assert ms[8] > 0.0
 
 
 @pytest.mark.parametrize("dist", [1, 2, 3])
