@@ -454,6 +454,25 @@ def test_kv_width_rule():
         vx.kv_sort(_d(np.zeros(10, dtype=np.int32)), _d(np.zeros(11, dtype=np.int32)))
 
 
+@pytest.mark.parametrize("kdt,vdt", [(np.int32, np.float32), (np.int32, np.uint32), (np.float64, np.float64),
+                                     (np.float64, np.int64)])
+def test_kv_value_dtypes_move_as_raw_bits(kdt, vdt):
+    """any same-width value type (keyvalue.py:44-47) rides
+    along bit for bit; sizes cover the finish and the CTA-local level."""
+    rng = np.random.default_rng(11)
+    for n in (3000, 1 << 20):
+        k = rng.integers(-5000, 5000, size=n).astype(kdt)
+        idx = np.arange(n)
+        v = (idx * 2.5).astype(vdt) if np.dtype(vdt).kind == "f" else idx.astype(vdt)
+        tk, tv = _d(k), _d(v)
+        vx.kv_sort(tk, tv)
+        gk, gv = _h(tk), _h(tv)
+        assert np.array_equal(gk, np.sort(k))
+        orig = (gv / 2.5).astype(np.int64) if np.dtype(vdt).kind == "f" else gv.astype(np.int64)
+        assert np.array_equal(np.sort(orig), idx)  # a permutation of the payloads
+        assert np.array_equal(k[orig], gk)  # every payload still sits next to its key
+
+
 def test_c4_reduced_digest_and_pairs(golden_dir):
     d = _digests(golden_dir)["c4_kv_2^18"]
     k0, v0 = inputs.c4_input(n=1 << 18)
