@@ -95,9 +95,14 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
         const uint64_t start = items[it].start;
         const unsigned len = (unsigned)items[it].len;
         const K* sk = src_k + start;
-        // ---- 1. key-code range
+        // ---- 1. key-code range: the parent's pivots bound an inner bucket;
+        //      the two outer buckets of a segment are measured
         U lo = ~(U)0, hi = 0;
-        {
+        const bool bounded = items[it].lo <= items[it].hi;
+        if (bounded) {
+            lo = (U)items[it].lo;
+            hi = (U)items[it].hi;
+        } else {
             unsigned i = tid;
             for (; i + 3 * NT < len; i += 4 * NT) {
                 U u[4];
@@ -114,7 +119,6 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
                 lo = ql_min(lo, u);
                 hi = ql_max(hi, u);
             }
-        }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             lo = ql_min(lo, (U)__shfl_xor_sync(0xffffffffu, lo, d));
@@ -129,6 +133,7 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
         for (int w = 0; w < (int)(NT / 32); ++w) {
             lo = ql_min(lo, sm.rmin[w]);
             hi = ql_max(hi, sm.rmax[w]);
+        }
         }
         if (lo == hi) {  // one key value: already sorted
             if (sk != out_k + start)
@@ -199,9 +204,42 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
                 ex += c[q];
             }
         }
-        // ---- 3. scatter into the other buffer, bucket-major, tile by tile
+        // ---- 3. scatter into the other buffer, bucket-major
         K* ok = oth_k + start;
         V* ov = KV ? oth_v + start : nullptr;
+        // keys only: every element straight to its bucket's fill cursor (a
+        // shared-memory atomic) -- order inside a bucket is irrelevant, the
+        // network sorts it, and the scattered stores merge in L2, so there
+        // are no tile barriers at all.  Pairs (two scattered stores per
+        // element) are staged per tile and written as runs instead
+        // (measured on B200: direct -4 % int32 keys, +26 % kv).
+        if constexpr (!KV) {
+        __syncthreads();  // cursors complete
+        {
+            unsigned i = tid;
+            for (; i + 3 * NT < len; i += 4 * NT) {
+                K x[4];
+                V y[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    x[r] = sk[i + r * NT];
+                    if constexpr (KV) y[r] = src_v[start + i + r * NT];
+                }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const unsigned pos = atomicAdd(&sm.off[bucket(x[r])], 1u);
+                    ok[pos] = x[r];
+                    if constexpr (KV) ov[pos] = y[r];
+                }
+            }
+            for (; i < len; i += NT) {
+                const K x = sk[i];
+                const unsigned pos = atomicAdd(&sm.off[bucket(x)], 1u);
+                ok[pos] = x;
+                if constexpr (KV) ov[pos] = src_v[start + i];
+            }
+        }
+        } else {
         for (unsigned t0 = 0; t0 < len; t0 += TILE) {
             const unsigned tn = min(TILE, len - t0);
 #pragma unroll
@@ -255,6 +293,7 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
                 if constexpr (KV) ov[pos] = sm.v[j];
             }
         }
+        }  // staged
         // ---- 4. every bucket through the bitonic network into the output
         if (tid == 0) sm.next = 0;
         __syncthreads();  // bucket runs written (CTA-scope visibility of global stores)

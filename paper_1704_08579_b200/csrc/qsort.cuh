@@ -73,6 +73,7 @@ struct Seg {
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
+    unsigned long long lo, hi;  // key-code bounds from the parent's pivots (lo > hi: unknown)
 };
 struct Fin {
     unsigned long long start;
@@ -486,7 +487,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                                                           Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
                                                           unsigned long long* __restrict__ bkt_pool,
                                                           Fin* __restrict__ fins, unsigned cap_seg, unsigned cap_fin,
-                                                          int dst_is_scratch, QlItemT* __restrict__ qls,
+                                                          int dst_is_scratch, const K* __restrict__ spl_pool,
+                                                          QlItemT* __restrict__ qls,
                                                           uint64_t ql_cap) {
     static_assert(kPlanNT >= kMaxBkt, "one thread per bucket");
     constexpr uint32_t LOCAL = FinCap<K, V>::value;
@@ -534,6 +536,15 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                     } else {
                         qls[q].start = bstart;
                         qls[q].len = c;
+                        // a range bucket 2j lies strictly between pivots j-1 and j
+                        const unsigned j = b >> 1;
+                        if (j > 0 && j < sg.m) {
+                            qls[q].lo = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j - 1]) + 1;
+                            qls[q].hi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
+                        } else {
+                            qls[q].lo = 1;
+                            qls[q].hi = 0;
+                        }
                     }
                 } else {
                     unsigned q = atomicAdd(&ctl_next->nseg, 1u);

@@ -266,7 +266,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
                 qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(segs[level & 1], c, ctl + level + 1,
                                                                  segs[(level + 1) & 1], bkt, fins[level & 1],
                                                                  (unsigned)lay.cap_seg, (unsigned)lay.cap_fin,
-                                                                 even ? 1 : 0, qls, ql_cap);
+                                                                 even ? 1 : 0, spl, qls, ql_cap);
             }
             VX_LAUNCHED();
             {
