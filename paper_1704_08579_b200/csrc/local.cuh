@@ -297,6 +297,16 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
         // ---- 4. every bucket through the bitonic network into the output
         if (tid == 0) sm.next = 0;
         __syncthreads();  // bucket runs written (CTA-scope visibility of global stores)
+#ifndef VX_QL_DYNAMIC
+        // buckets are near-equal (interpolation over a narrow range), so warps
+        // take them round-robin: no shared counter between networks
+        for (unsigned b0 = warp; b0 < nb; b0 += NT / 32) {
+            const unsigned cb = sm.cnt[b0];
+            if (cb == 0) continue;
+            const unsigned bs = sm.off[b0] - cb;  // the cursor ended at the bucket's end
+            warp_sort_any<K, V>(ok, ov, out_k + start, KV ? out_v + start : nullptr, bs, cb);
+        }
+#else
         for (;;) {
             unsigned b0 = 0;
             if (lane == 0) b0 = atomicAdd(&sm.next, 1u);
@@ -307,6 +317,7 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
             const unsigned bs = sm.off[b0] - cb;  // the cursor ended at the bucket's end
             warp_sort_any<K, V>(ok, ov, out_k + start, KV ? out_v + start : nullptr, bs, cb);
         }
+#endif
         done += len;
         __syncthreads();
     }
