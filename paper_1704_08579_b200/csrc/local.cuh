@@ -69,6 +69,39 @@ struct QlSmem {
 };
 
 
+// f(key) for every key of p[0, len): 16-byte vector loads for the aligned
+// body, four vectors in flight per thread, scalar head and tail.
+template <typename K, unsigned NT, typename F>
+__device__ __forceinline__ void seg_for_each(const K* __restrict__ p, unsigned len, F&& f) {
+    constexpr unsigned VE = 16 / sizeof(K);
+    union Vec {
+        uint4 v;
+        K k[VE];
+    };
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const unsigned head = min(len, (unsigned)(((16 - (a & 15)) & 15) / sizeof(K)));
+    for (unsigned i = threadIdx.x; i < head; i += NT) f(p[i]);
+    const unsigned nv = (len - head) / VE;
+    const uint4* v = reinterpret_cast<const uint4*>(p + head);
+    unsigned j = threadIdx.x;
+    for (; j + 3 * NT < nv; j += 4 * NT) {
+        Vec w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u].v = v[j + u * NT];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (unsigned r = 0; r < VE; ++r) f(w[u].k[r]);
+    }
+    for (; j < nv; j += NT) {
+        Vec w;
+        w.v = v[j];
+#pragma unroll
+        for (unsigned r = 0; r < VE; ++r) f(w.k[r]);
+    }
+    for (unsigned i = head + nv * VE + threadIdx.x; i < len; i += NT) f(p[i]);
+}
+
 template <typename U>
 __device__ __forceinline__ U ql_min(U a, U b) { return a < b ? a : b; }
 template <typename U>
@@ -162,17 +195,7 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
 #pragma unroll
         for (unsigned q = 0; q < BPT; ++q) sm.cnt[tid * BPT + q] = 0;
         __syncthreads();
-        {
-            unsigned i = tid;
-            for (; i + 3 * NT < len; i += 4 * NT) {
-                K x[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) x[r] = sk[i + r * NT];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) atomicAdd(&sm.cnt[bucket(x[r])], 1u);
-            }
-            for (; i < len; i += NT) atomicAdd(&sm.cnt[bucket(sk[i])], 1u);
-        }
+        seg_for_each<K, NT>(sk, len, [&](K x) { atomicAdd(&sm.cnt[bucket(x)], 1u); });
         __syncthreads();
         unsigned c[BPT], sum = 0;
         bool over = false;
@@ -215,30 +238,7 @@ __global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlI
         // (measured on B200: direct -4 % int32 keys, +26 % kv).
         if constexpr (!KV) {
         __syncthreads();  // cursors complete
-        {
-            unsigned i = tid;
-            for (; i + 3 * NT < len; i += 4 * NT) {
-                K x[4];
-                V y[4];
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    x[r] = sk[i + r * NT];
-                    if constexpr (KV) y[r] = src_v[start + i + r * NT];
-                }
-#pragma unroll
-                for (int r = 0; r < 4; ++r) {
-                    const unsigned pos = atomicAdd(&sm.off[bucket(x[r])], 1u);
-                    ok[pos] = x[r];
-                    if constexpr (KV) ov[pos] = y[r];
-                }
-            }
-            for (; i < len; i += NT) {
-                const K x = sk[i];
-                const unsigned pos = atomicAdd(&sm.off[bucket(x)], 1u);
-                ok[pos] = x;
-                if constexpr (KV) ov[pos] = src_v[start + i];
-            }
-        }
+        seg_for_each<K, NT>(sk, len, [&](K x) { ok[atomicAdd(&sm.off[bucket(x)], 1u)] = x; });
         } else {
         for (unsigned t0 = 0; t0 < len; t0 += TILE) {
             const unsigned tn = min(TILE, len - t0);
