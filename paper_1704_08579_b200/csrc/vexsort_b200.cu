@@ -204,8 +204,10 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     const unsigned leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
     QlItemT* qls = reinterpret_cast<QlItemT*>(w + lay.off_ql);
 #ifndef VX_NO_QL
-    // the CTA-local level needs leaves of ~2x its bucket target (skipped for a small sort_bound)
-    const bool ql_on = leaf >= 2 * QlCfg<K, V>::LT;
+    // the CTA-local level needs leaves of ~2x its bucket target (skipped for a
+    // small sort_bound) and enough segments to fill the GPU (one CTA each):
+    // below ~256 target-sized segments the finish path alone is faster
+    const bool ql_on = leaf >= 2 * QlCfg<K, V>::LT && n >= 256 * QlCfg<K, V>::TARGET;
 #else
     const bool ql_on = false;
 #endif
