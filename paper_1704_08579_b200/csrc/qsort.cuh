@@ -341,6 +341,60 @@ __device__ __forceinline__ void cta_bitonic(K* a, V* av, unsigned P) {
     }
 }
 
+// Sort S (pow2, 256..4096) samples in shared memory with the CTA: each warp
+// sorts a 256-sample chunk in registers (the warp bitonic network), then
+// every sample's global rank is its position in its chunk plus its
+// lower/upper bound in every other chunk (ties broken by chunk), and the
+// samples move to their ranks.  One network pass and one merge instead of
+// log^2(S) CTA-wide compare-exchange rounds.
+template <typename K>
+__device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
+    constexpr unsigned C = 256, E = C / 32, MAXW = kMaxSample / C;
+    static_assert(kPlanNT / 32 >= MAXW, "one warp per chunk");
+    const unsigned W = S / C, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < W) {
+        K k[E];
+        NoVal v[E];
+#pragma unroll
+        for (unsigned r = 0; r < E; ++r) k[r] = s[warp * C + lane * E + r];
+        WarpBitonic<K, NoVal, E>::sort(k, v);
+#pragma unroll
+        for (unsigned r = 0; r < E; ++r) s[warp * C + lane * E + r] = k[r];
+    }
+    __syncthreads();
+    if (W == 1) return;
+    constexpr unsigned PER = kMaxSample / kPlanNT;
+    K val[PER];
+    unsigned rk[PER];
+#pragma unroll
+    for (unsigned q = 0; q < PER; ++q) {
+        const unsigned i = q * kPlanNT + threadIdx.x;
+        if (i < S) {
+            const K v = s[i];
+            const unsigned c = i / C;
+            unsigned pos = i % C;
+            for (unsigned o = 0; o < W; ++o) {
+                if (o == c) continue;
+                const K* ch = s + o * C;
+                unsigned lo = 0, hi = C;  // o < c: count(<= v); o > c: count(< v)
+                while (lo < hi) {
+                    const unsigned mid = (lo + hi) >> 1;
+                    const bool before = o < c ? !(v < ch[mid]) : (ch[mid] < v);
+                    if (before) lo = mid + 1; else hi = mid;
+                }
+                pos += lo;
+            }
+            val[q] = v;
+            rk[q] = pos;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (unsigned q = 0; q < PER; ++q)
+        if (q * kPlanNT + threadIdx.x < S) s[rk[q]] = val[q];
+    __syncthreads();
+}
+
 // ------------------------------------------------------------ init
 __global__ void qs_init_kernel(Seg* segs, Ctl* ctl, unsigned long long n) {
     segs[0].start = 0;
@@ -384,7 +438,11 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             s_samp[i] = src[start + (h % len)];
         }
         __syncthreads();
+#ifdef VX_PLAN_CTA_BITONIC
         cta_bitonic<K, NoVal, kPlanNT>(s_samp, nullptr, S);
+#else
+        plan_sort_samples<K>(s_samp, S);
+#endif
         // candidate j = sample at quantile (j+1)/(mt+1); keep distinct values
         K cand = K();
         unsigned keep = 0;
