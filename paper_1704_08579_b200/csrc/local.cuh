@@ -39,7 +39,11 @@ constexpr unsigned kQlLeafTarget = VX_QL_LT;  // mean interpolation bucket (int3
 template <typename K, typename V>
 struct QlCfg {
     static constexpr unsigned BYTES = sizeof(K) + (HasVal<V>::value ? sizeof(V) : 0);
-    static constexpr uint64_t TARGET = VX_QL_TARGET_BYTES / BYTES;  // plan aims level leaves here
+    static constexpr uint64_t TARGET = VX_QL_TARGET_BYTES / BYTES;  // plan aims level leaves here (at most)
+#ifndef VX_QL_TMIN_BYTES
+#define VX_QL_TMIN_BYTES (192 * 1024)
+#endif
+    static constexpr uint64_t TMIN = VX_QL_TMIN_BYTES / BYTES;      // ... and at least here
     static constexpr uint64_t CAP = 3 * TARGET;                     // largest segment taken
     static constexpr unsigned IPT = 8;
     static constexpr unsigned TILE = kQlNT * IPT;

@@ -4,6 +4,7 @@
 // qsort.cuh) are instantiated here for the element kinds of the reference
 // (int32, float64) and their same-width payloads (uint32 / uint64).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -211,7 +212,16 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
 #else
     const bool ql_on = false;
 #endif
-    const uint64_t ql_target = ql_on ? QlCfg<K, V>::TARGET : 0, ql_cap = ql_on ? QlCfg<K, V>::CAP : 0;
+    // leaves as small as the level count allows (L2 residency of the
+    // CTA-local working set): the levels needed at the full target, then
+    // the smallest target in [TMIN, TARGET] that needs no more of them
+    uint64_t ql_target = 0;
+    if (ql_on) {
+        const double L = ceil(log((double)n / (double)QlCfg<K, V>::TARGET) / log(256.0) - 1e-9);
+        const double t = (double)n / pow(256.0, L < 1.0 ? 1.0 : L);
+        ql_target = (uint64_t)std::min((double)QlCfg<K, V>::TARGET, std::max((double)QlCfg<K, V>::TMIN, ceil(t)));
+    }
+    const uint64_t ql_cap = ql_on ? QlCfg<K, V>::CAP : 0;
     if (!HasVal<V>::value) sv = nullptr;
 
     const int sms = num_sms();
