@@ -112,7 +112,10 @@ template <typename U>
 __device__ __forceinline__ U ql_max(U a, U b) { return a > b ? a : b; }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQlNT, 2048 / kQlNT) qs_local_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
+#ifndef VX_QL_MINB
+#define VX_QL_MINB (2048 / kQlNT)
+#endif
+__global__ void __launch_bounds__(kQlNT, VX_QL_MINB) qs_local_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
                                                             Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
                                                             unsigned cap_seg, const K* __restrict__ src_k,
                                                             const V* __restrict__ src_v, K* __restrict__ oth_k,
