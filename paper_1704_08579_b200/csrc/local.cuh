@@ -111,11 +111,15 @@ __device__ __forceinline__ U ql_min(U a, U b) { return a < b ? a : b; }
 template <typename U>
 __device__ __forceinline__ U ql_max(U a, U b) { return a > b ? a : b; }
 
+// Resident CTAs per SM: keys-only sorts run one 1024-thread CTA per SM (64
+// registers, half the L2 footprint); pairs keep two (their tile-staged
+// scatter hides more latency with the second CTA).  Measured on B200.
+template <typename V>
+struct QlMinBlocks {
+    static constexpr int value = HasVal<V>::value ? 2048 / kQlNT : 1;
+};
 template <typename K, typename V>
-#ifndef VX_QL_MINB
-#define VX_QL_MINB (2048 / kQlNT)
-#endif
-__global__ void __launch_bounds__(kQlNT, VX_QL_MINB) qs_local_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
                                                             Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
                                                             unsigned cap_seg, const K* __restrict__ src_k,
                                                             const V* __restrict__ src_v, K* __restrict__ oth_k,
