@@ -2,18 +2,19 @@
 // segments (north-star subsystem 3, the bottom of _kernels.quicksort,
 // _kernels.py:396-423).
 //
-// A segment of up to QlCap elements (~256 KB at the mean) is owned by one CTA
-// from partition to sorted output, so its working set stays in L2:
-//   1. one pass for the key-code range [min, max] of the segment (HBM read);
-//   2. one pass counting interpolation buckets of ~LT keys over that range
-//      (equal-width code intervals = evenly spaced pivots), read from L2;
+// A segment of up to QlCfg::CAP keys (48-64 Ki int32 at the mean) is owned
+// by one CTA from partition to sorted output, so its working set stays in L2:
+//   1. the key-code range: the parent's pivots bound an inner bucket; the
+//      two outer buckets of a segment take one pass for [min, max];
+//   2. one pass (the HBM read) counting interpolation buckets of ~LT keys
+//      over that range (equal-width code intervals = evenly spaced pivots);
 //      if any bucket exceeds the leaf bound the keys are skewed and the
 //      segment goes back to the sampled-pivot level queue instead;
-//   3. one pass that classifies again, ranks inside the tile, stages the
-//      tile bucket-major in shared memory and writes every bucket run to its
-//      place in the other buffer (CTA-local cursors, no global atomics);
-//   4. warps sort the buckets (<= leaf bound) with the register bitonic
-//      network (bitonic.cuh) straight into the output array.
+//   3. one pass (from L2) that classifies again and places every key in its
+//      bucket of the other buffer: keys only straight to the bucket's
+//      shared-memory cursor, pairs staged per tile and written as runs;
+//   4. warps take the buckets round-robin and sort each (<= leaf bound) with
+//      the register bitonic network (bitonic.cuh) straight into the output.
 // This replaces the last global level (plan + hist + scatter over the whole
 // array) and the finish kernel's own partition for every segment it takes.
 #pragma once
