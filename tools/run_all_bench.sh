@@ -12,10 +12,10 @@ for w in sort_i32 sort_f64 c1 c2_i32 c2_f64 c3 c4 c5_f64_uniform; do
   timeout 600 python bench.py --workload $w --steps $S --warmup $W > gpurun_out/all/$w.json 2> gpurun_out/all/$w.err
   echo "$w rc=$?"
 done
-for d in sorted reverse few; do
-  timeout 600 python bench.py --workload c5_i32_$d --steps $S --warmup $W --no-e2e > gpurun_out/all/c5_i32_$d.json 2> gpurun_out/all/c5_i32_$d.err
-  echo "c5_i32_$d rc=$?"
-done
+for t in i32 f64; do for d in sorted reverse few; do
+  timeout 600 python bench.py --workload c5_${t}_$d --steps $S --warmup $W --no-e2e > gpurun_out/all/c5_${t}_$d.json 2> gpurun_out/all/c5_${t}_$d.err
+  echo "c5_${t}_$d rc=$?"
+done; done
 python - <<'PY'
 import glob, json, os
 for f in sorted(glob.glob("gpurun_out/all/*.json")):
