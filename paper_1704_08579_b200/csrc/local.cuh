@@ -201,6 +201,10 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
         if ((uint64_t)r32 + 1 <= nb) nb = r32 + 1;
         else mul = (uint32_t)(((uint64_t)nb << 32) / ((uint64_t)r32 + 1));
         auto bucket = [&](K key) -> unsigned {
+#ifdef VX_CHECK
+            // checked build: every key lies inside the segment's bounds
+            if (OKey<K>::of(key) < lo || OKey<K>::of(key) > hi) __trap();
+#endif
             const uint32_t d = (uint32_t)((OKey<K>::of(key) - lo) >> sh);
             return mul ? __umulhi(d, mul) : d;
         };
