@@ -48,10 +48,13 @@ struct QlCfg {
     static constexpr uint64_t CAP = 3 * TARGET;                     // largest segment taken
     static constexpr unsigned IPT = 8;
     static constexpr unsigned TILE = kQlNT * IPT;
-    static constexpr unsigned LT = BYTES <= 4 ? kQlLeafTarget : kQlLeafTarget / 2;
-    static constexpr unsigned NB = 2048;  // bucket table capacity (>= CAP / LT)
+#ifndef VX_QL_LT8
+#define VX_QL_LT8 55
+#endif
+    static constexpr unsigned LT = BYTES <= 4 ? kQlLeafTarget : VX_QL_LT8;  // mean bucket (8-byte elements: smaller)
+    static constexpr unsigned NB = CAP / LT + 1 <= 2048 ? 2048 : 4096;     // bucket table capacity (>= CAP / LT)
     static constexpr unsigned BPT = NB / kQlNT;
-    static_assert(CAP / (BYTES <= 4 ? kQlLeafTarget : kQlLeafTarget / 2) + 1 <= NB, "bucket table too small");
+    static_assert(CAP / LT + 1 <= NB, "bucket table too small");
 };
 
 using QlItem = QlItemT;
