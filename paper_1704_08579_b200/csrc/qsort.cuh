@@ -363,29 +363,42 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
     }
     __syncthreads();
     if (W == 1) return;
+    // every thread ranks its PER samples in lockstep: fixed-step branch-free
+    // searches, PER independent shared loads per step (the CTA is alone on
+    // its SM at level 0, so latency is hidden by ILP, not by other warps)
     constexpr unsigned PER = kMaxSample / kPlanNT;
+    const unsigned per = (S + kPlanNT - 1) / kPlanNT;  // samples this thread really ranks
     K val[PER];
-    unsigned rk[PER];
+    unsigned rk[PER], ch_of[PER];
 #pragma unroll
     for (unsigned q = 0; q < PER; ++q) {
-        const unsigned i = q * kPlanNT + threadIdx.x;
-        if (i < S) {
-            const K v = s[i];
-            const unsigned c = i / C;
-            unsigned pos = i % C;
-            for (unsigned o = 0; o < W; ++o) {
-                if (o == c) continue;
-                const K* ch = s + o * C;
-                unsigned lo = 0, hi = C;  // o < c: count(<= v); o > c: count(< v)
-                while (lo < hi) {
-                    const unsigned mid = (lo + hi) >> 1;
-                    const bool before = o < c ? !(v < ch[mid]) : (ch[mid] < v);
-                    if (before) lo = mid + 1; else hi = mid;
-                }
-                pos += lo;
+        const unsigned i = min(q * kPlanNT + threadIdx.x, S - 1);
+        val[q] = s[i];
+        ch_of[q] = i / C;
+        rk[q] = i % C;
+    }
+    for (unsigned o = 0; o < W; ++o) {
+        const K* ch = s + o * C;
+        unsigned lo[PER];
+#pragma unroll
+        for (unsigned q = 0; q < PER; ++q) lo[q] = 0;
+        // o < c: count(<= v); o > c: count(< v) -- ties ordered by chunk
+#pragma unroll
+        for (unsigned step = C / 2; step > 0; step >>= 1) {
+#pragma unroll
+            for (unsigned q = 0; q < PER; ++q) {
+                if (q >= per) break;
+                const K e = ch[lo[q] + step - 1];
+                const bool before = o < ch_of[q] ? !(val[q] < e) : (e < val[q]);
+                lo[q] += before ? step : 0u;
             }
-            val[q] = v;
-            rk[q] = pos;
+        }
+#pragma unroll
+        for (unsigned q = 0; q < PER; ++q) {
+            if (q >= per) break;
+            const K e = ch[lo[q]];  // lo <= C - 1 here
+            const bool before = o < ch_of[q] ? !(val[q] < e) : (e < val[q]);
+            if (o != ch_of[q]) rk[q] += lo[q] + (before ? 1u : 0u);
         }
     }
     __syncthreads();
@@ -433,9 +446,10 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         }
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
+#pragma unroll 4
         for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
             const uint64_t h = mix64(seed ^ mix64(start * 0x9E3779B97F4A7C15ULL + i));
-            s_samp[i] = src[start + (h % len)];
+            s_samp[i] = src[start + __umul64hi(h, len)];  // uniform in [0, len) without a 64-bit division
         }
         __syncthreads();
 #ifdef VX_PLAN_CTA_BITONIC
