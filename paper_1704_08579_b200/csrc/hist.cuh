@@ -85,8 +85,16 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     }
     __syncthreads();
 
-    unsigned cur = 0xffffffffu, bkt_off = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, rsh = 0;
+    bool radix = false;
+    U rlo = 0;
     CellParams<U> cp{};
+    // radix-mode segments: bucket = (code - lo) >> shift (clamped: keys lie
+    // in [lo, hi] by construction)
+    auto classify = [&](K key) -> unsigned {
+        if (radix) return (unsigned)min((U)(nb - 1), (U)((OKey<K>::of(key) - rlo) >> rsh));
+        return ct_classify(s_ct, cp, key);
+    };
     unsigned stage = 0, par = 0;          // this tile's stage and phase parity
     unsigned pstage = NS - 1, ppar = 1;   // the previous tile's
     for (unsigned t = t0; t < t1; ++t) {
@@ -101,13 +109,17 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             // flush the previous segment's counts, build the new table
             __syncthreads();
             if (cur != 0xffffffffu)
-                for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT)
+                for (unsigned b = tid; b < nb; b += kQsNT)
                     if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
             cur = bt.seg;
             const Seg sg = segs[bt.seg];
             bkt_off = sg.bkt_off;
-            cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
-            for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT) s_hist[b] = 0;
+            nb = sg.nb;
+            radix = sg.mode == 1;
+            rlo = (U)sg.lo;
+            rsh = sg.shift;
+            if (!radix) cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
+            for (unsigned b = tid; b < nb; b += kQsNT) s_hist[b] = 0;
             __syncthreads();
         }
         const char* buf = reinterpret_cast<const char*>(smem_raw) + stage * BUF;
@@ -115,7 +127,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             const K* sb = reinterpret_cast<const K*>(buf + bt.shift);
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
-                const unsigned b = ct_classify(s_ct, cp, sb[i * kQsNT + tid]);
+                const unsigned b = classify(sb[i * kQsNT + tid]);
                 atomicAdd(&s_hist[b], 1u);
                 ids[bt.base + i * kQsNT + tid] = (unsigned short)b;
             }
@@ -125,7 +137,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                 const unsigned idx = i * kQsNT + tid;
                 if (idx < bt.tn) {
                     const K x = tile_get<K>(buf, bt, src, idx);
-                    const unsigned b = ct_classify(s_ct, cp, x);
+                    const unsigned b = classify(x);
                     atomicAdd(&s_hist[b], 1u);
                     ids[bt.base + idx] = (unsigned short)b;
                 }
@@ -140,7 +152,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
         }
     }
     __syncthreads();
-    for (unsigned b = tid; b < 2 * cp.m + 1; b += kQsNT)
+    for (unsigned b = tid; b < nb; b += kQsNT)
         if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
 }
 

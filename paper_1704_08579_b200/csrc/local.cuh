@@ -233,6 +233,8 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
                 } else {
                     next_segs[q].start = start;
                     next_segs[q].len = len;
+                    next_segs[q].lo = 1;  // skewed: sampled pivots next
+                    next_segs[q].hi = 0;
                 }
             }
             continue;  // the barrier above ends every use of the tables

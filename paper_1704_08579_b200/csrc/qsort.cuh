@@ -67,9 +67,16 @@ struct FinCap {
     static constexpr uint32_t value = bytes_per <= 4 ? 8192 : (bytes_per <= 8 ? 6144 : 3072);
 };
 
+// A level segment.  mode 0: partitioned around m sampled pivots into
+// nb = 2m+1 buckets (ranges and equal-to-pivot buckets).  mode 1 (a segment
+// whose key-code bounds [lo, hi] are known from its parent): nb buckets of
+// 2^shift consecutive codes each, bucket = (code - lo) >> shift -- evenly
+// spaced pivots, classified with a subtract and a shift.
 struct Seg {
     unsigned long long start, len;
     unsigned spl_off, m, bkt_off, tile_base;
+    unsigned long long lo, hi;  // key-code bounds (lo > hi: unknown)
+    unsigned nb, shift, mode, pad_;
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -412,6 +419,8 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
 __global__ void qs_init_kernel(Seg* segs, Ctl* ctl, unsigned long long n) {
     segs[0].start = 0;
     segs[0].len = n;
+    segs[0].lo = 1;
+    segs[0].hi = 0;
     ctl[0].nseg = 1;
 }
 
@@ -444,6 +453,52 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             const double f = ceil(pow(r, 1.0 / (L < 1.0 ? 1.0 : L)) - 1e-9);
             mt = (unsigned)max(2.0, min((double)kMaxSplit, f - 1.0));
         }
+        using U = typename OKey<K>::U;
+        const uint64_t slo = segs[s].lo, shi = segs[s].hi;
+        (void)slo;
+        (void)shi;
+#ifndef VX_RADIX_SPAN
+#define VX_RADIX_SPAN 1
+#endif
+#ifndef VX_NO_RADIX
+        // 4-byte keys only: float64 codes change density at every binade,
+        // which unbalances equal-width buckets (measured slower)
+        if (sizeof(K) == 4 && slo < shi) {
+            // bounds known from the parent: 2^shift-code buckets over
+            // [lo, hi], at most 2(mt+1) of them (at least half non-empty
+            // for locally uniform keys) -- no sample, no pivot table
+            const uint64_t range = (uint64_t)(U)(shi - slo);
+            const uint64_t want = (uint64_t)VX_RADIX_SPAN * (mt + 1);
+            const uint64_t bmax = want < (uint64_t)kMaxBkt ? want : (uint64_t)kMaxBkt;
+            unsigned sh = 0;
+            while ((range >> sh) + 1 > bmax) ++sh;
+            const unsigned nb = (unsigned)((range >> sh) + 1);
+            if (threadIdx.x == 0) {
+                const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
+                unsigned bo = atomicAdd(&ctl->bkt_ctr, nb);
+                unsigned to = atomicAdd(&ctl->tile_ctr, ntiles);
+                if (bo + nb > cap_bkt || to + ntiles > cap_tiles) {
+                    atomicOr(&ctl->err, kErrCapacity);
+                    bo = to = 0;
+                }
+                s_off[1] = bo;
+                s_off[2] = to;
+                segs[s].spl_off = 0;
+                segs[s].m = 0;
+                segs[s].bkt_off = bo;
+                segs[s].tile_base = to;
+                segs[s].nb = nb;
+                segs[s].shift = sh;
+                segs[s].mode = 1;
+            }
+            __syncthreads();
+            for (unsigned b = threadIdx.x; b < nb; b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
+            const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
+            for (unsigned t = threadIdx.x; t < ntiles; t += kPlanNT) tile_owner[s_off[2] + t] = s;
+            __syncthreads();
+            continue;
+        }
+#endif
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
 #pragma unroll 4
@@ -487,6 +542,9 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             segs[s].m = m;
             segs[s].bkt_off = bo;
             segs[s].tile_base = to;
+            segs[s].nb = 2 * m + 1;
+            segs[s].shift = 0;
+            segs[s].mode = 0;
         }
         __syncthreads();
         if (keep) spl_pool[s_off[0] + rank] = cand;
@@ -568,15 +626,35 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
     const unsigned nseg = ctl->nseg;
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const Seg sg = segs[s];
-        const unsigned nb = 2 * sg.m + 1;
+        const unsigned nb = sg.nb;
+        const bool radix = sg.mode == 1;
         const unsigned b = threadIdx.x;
         const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + b] : 0ull;
         const unsigned long long ex = block_excl_scan_u64<kPlanNT>(c, s_scan);
         if (b < nb) {
             const unsigned long long bstart = sg.start + ex;
             bkt_pool[sg.bkt_off + b] = bstart;  // becomes the scatter cursor
+            // the bucket's key-code bounds, for the child's own partition:
+            // a range bucket 2j lies strictly between pivots j-1 and j; a
+            // radix bucket spans its 2^shift codes.  A radix child holding
+            // more than half its parent is skewed: it forgets its bounds
+            // and is partitioned around sampled pivots.
+            unsigned long long clo = 1, chi = 0;
+            if (radix) {
+                const unsigned long long w = 1ull << sg.shift;
+                clo = sg.lo + (unsigned long long)b * w;
+                chi = b + 1 < nb ? sg.lo + (unsigned long long)(b + 1) * w - 1 : sg.hi;
+                if (2 * c > sg.len) {
+                    clo = 1;
+                    chi = 0;
+                }
+            } else if (!(b & 1u) && (b >> 1) > 0 && (b >> 1) < sg.m) {
+                const unsigned j = b >> 1;
+                clo = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j - 1]) + 1;
+                chi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
+            }
             if (c > 0) {
-                const bool final_ = (b & 1u) || c == 1;
+                const bool final_ = c == 1 || (radix ? (sg.shift == 0) : (b & 1u) != 0);
                 if (final_) {
                     if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
                         const unsigned nch = (unsigned)((c + kCopyChunk - 1) / kCopyChunk);
@@ -608,15 +686,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                     } else {
                         qls[q].start = bstart;
                         qls[q].len = c;
-                        // a range bucket 2j lies strictly between pivots j-1 and j
-                        const unsigned j = b >> 1;
-                        if (j > 0 && j < sg.m) {
-                            qls[q].lo = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j - 1]) + 1;
-                            qls[q].hi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
-                        } else {
-                            qls[q].lo = 1;
-                            qls[q].hi = 0;
-                        }
+                        qls[q].lo = clo;
+                        qls[q].hi = chi;
                     }
                 } else {
                     unsigned q = atomicAdd(&ctl_next->nseg, 1u);
@@ -625,6 +696,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                     } else {
                         next_segs[q].start = bstart;
                         next_segs[q].len = c;
+                        next_segs[q].lo = clo;
+                        next_segs[q].hi = chi;
                     }
                 }
             }

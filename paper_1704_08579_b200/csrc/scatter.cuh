@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         if (g.seg != cur) {
             cur = g.seg;
             bkt_off = segs[g.seg].bkt_off;
-            nb = 2 * segs[g.seg].m + 1;
+            nb = segs[g.seg].nb;
         }
         unsigned* cnt = sm.cnt[p];
         moved += g.tn;
