@@ -9,17 +9,22 @@
 // the boundary, the two side predicates and the multisets.
 //
 // B200 design, one HBM read + one HBM write per element:
-//  * dynamic tile ids (global atomic) so every predecessor tile is resident
-//    -> decoupled look-back always makes progress;
+//  * small tiles (128 threads x 16 elements) so ~10 CTAs share an SM and
+//    one tile's loads overlap another's staging and stores;
 //  * 128-bit vector loads (int4 / double2) striped across the CTA;
 //  * classify + rank lows AND valid elements with ONE packed 16|16-bit
 //    block scan (warp shuffles, then warp totals);
-//  * decoupled look-back on the low count only, 64-bit descriptors
-//    {status:2 | inclusive:62} published with st.release / read with
-//    ld.acquire, 32 predecessors per warp step;
-//  * highs need no second scan: H_excl(t) = t*T - L_excl(t); they fill the
-//    array from the right end (the reference's right_w cursor at tile
-//    granularity, _kernels.py:197-212), so the split is never needed early;
+//  * tile offsets from two run cursors (the reference's left_w / right_w
+//    cursors, _kernels.py:197-212, at tile granularity): one atomic reserves
+//    the tile's lows at the left end, one its highs from the right end, so no
+//    tile ever waits on another; the cursors sit on separate L2 lines.  The
+//    order of the runs inside each side follows reservation order (sides,
+//    split and multisets are fixed; the layout was never the reference's);
+//  * build option VX_PART_LOOKBACK: deterministic tile-ordered layout via a
+//    decoupled look-back on the low count (64-bit {status:2 | inclusive:62}
+//    descriptors, st.release / ld.acquire, 32 predecessors per warp step,
+//    dynamic tile ids; highs at H_excl(t) = t*T - L_excl(t)) -- 1.8x slower
+//    on B200 because its per-tile latency needs big tiles, i.e. one CTA/SM;
 //  * the tile is staged in shared memory as [lows | highs] and written as two
 //    contiguous runs with consecutive threads -> coalesced stores.
 #pragma once
@@ -118,9 +123,14 @@ __global__ void __launch_bounds__(NT) partition2_kernel(const K* __restrict__ ki
     __shared__ unsigned long long s_excl;
 
     const int tid = threadIdx.x;
+#ifdef VX_PART_LOOKBACK
     if (tid == 0) s_tile = atomicAdd(counter, 1u);
     __syncthreads();
     const uint64_t tile = s_tile;
+#else
+    (void)s_tile;
+    const uint64_t tile = blockIdx.x;  // no tile waits on another: launch order is enough
+#endif
     const uint64_t base = tile * (uint64_t)T;
     const uint64_t ntiles = (n + T - 1) / T;
     const unsigned tn = (unsigned)min((uint64_t)T, n - base);
@@ -169,10 +179,20 @@ __global__ void __launch_bounds__(NT) partition2_kernel(const K* __restrict__ ki
     unsigned rl = packed & 0xffffu;
     unsigned rh = L_t + ((packed >> 16) - rl);
 
+#ifndef VX_PART_LOOKBACK
+    // run cursors instead of the look-back: each tile reserves its lows at
+    // the left cursor and its highs at the right cursor (layout order then
+    // follows reservation order, not tile order)
+    __shared__ unsigned long long s_hexcl;
+    unsigned long long* cur = reinterpret_cast<unsigned long long*>(counter);  // lo, hi, done: one L2 line each
+    if (tid == 0) s_excl = atomicAdd(&cur[0], (unsigned long long)L_t);
+    if (tid == 32) s_hexcl = atomicAdd(&cur[16], (unsigned long long)H_t);
+#else
     if (tid < 32) {
         const unsigned long long ex = lookback_excl(state, tile, L_t);
         if (tid == 0) s_excl = ex;
     }
+#endif
 
     // stage [lows | highs] in shared memory
 #pragma unroll
@@ -186,14 +206,28 @@ __global__ void __launch_bounds__(NT) partition2_kernel(const K* __restrict__ ki
     __syncthreads();
 
     const uint64_t L_excl = s_excl;
+#ifndef VX_PART_LOOKBACK
+    const uint64_t H_excl = s_hexcl;
+#else
     const uint64_t H_excl = base - L_excl;  // every preceding tile is full
+#endif
     const uint64_t hi_base = n - H_excl - H_t;
     for (unsigned j = tid; j < N_t; j += NT) {
         const uint64_t dst = j < L_t ? L_excl + j : hi_base + (j - L_t);
         kout[dst] = sk[j];
         if constexpr (KV) vout[dst] = sv[j];
     }
+#ifndef VX_PART_LOOKBACK
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(reinterpret_cast<unsigned*>(&cur[32]), 1u) == (unsigned)(ntiles - 1)) {
+            __threadfence();
+            *d_split = atomicAdd(&cur[0], 0ull);
+        }
+    }
+#else
     if (tile == ntiles - 1 && tid == 0) *d_split = L_excl + L_t;
+#endif
 }
 
 }  // namespace vx

@@ -325,17 +325,29 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
 }
 
 // -------------------------------------------------------------- partition
-// Tile shape of the pivot partition.  Measured on B200 (c3, 2^28 f64):
-// 256x8 2.36 ms, 256x16 1.45-1.50, 512x16 1.35, 256x32 1.39, 1024x16 1.24 ms
-// -- larger tiles win (fewer look-back links per element).  Staging must fit
-// in shared memory, so 16-byte pairs use half the tile.
+// Tile shape of the pivot partition.  Measured on B200 (c3, 2^28 f64,
+// kernel time).  With the decoupled look-back (VX_PART_LOOKBACK): 256x8
+// 2.36 ms, 256x16 1.45, 512x16 1.30, 1024x16 1.19 -- larger tiles win, the
+// look-back latency is exposed once per tile.  With run cursors (default):
+// 1024x16 0.98, 512x16 0.77, 256x16 0.69, 128x16 0.67 ms (97 % of HBM
+// peak), 128x32 0.70, 256x8 0.76 -- small tiles keep many CTAs per SM, so
+// loads of one tile overlap the staging and stores of another.  The three
+// cursors sit on separate L2 lines (on one line 128x16 ran 1.50 ms: the
+// same-line atomics serialise).  Staging must fit in shared memory, so
+// 16-byte pairs use half the tile.
 template <typename K, typename V>
 struct PartCfg {
     static constexpr int BYTES = sizeof(K) + (HasVal<V>::value ? sizeof(V) : 0);
-    static constexpr int NT = 1024;
-    static constexpr int IPT = BYTES <= 8 ? 16 : 8;
+#ifndef VX_PART_NT
+#define VX_PART_NT 128
+#endif
+#ifndef VX_PART_IPT
+#define VX_PART_IPT 16
+#endif
+    static constexpr int NT = VX_PART_NT;
+    static constexpr int IPT = BYTES <= 8 ? VX_PART_IPT : VX_PART_IPT / 2;
 };
-constexpr uint64_t kPartMinTile = 1024 * 8;
+constexpr uint64_t kPartMinTile = (uint64_t)VX_PART_NT * (VX_PART_IPT / 2);
 
 template <typename K, typename V>
 int run_partition(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, K pivot, int64_t* d_split, void* ws,
@@ -347,11 +359,15 @@ int run_partition(const K* kin, const V* vin, K* kout, V* vout, uint64_t n, K pi
         return VX_OK;
     }
     const uint64_t ntiles = (n + T - 1) / T;
-    const size_t need = align_up(ntiles * 8) + 256;
+    const size_t need = align_up(ntiles * 8) + 512;
     if (!ws || ws_bytes < need) return fail(VX_EWORKSPACE, "partition workspace too small");
     auto* state = static_cast<unsigned long long*>(ws);
     auto* counter = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up(ntiles * 8));
+#ifdef VX_PART_LOOKBACK
     VX_CUDA(cudaMemsetAsync(ws, 0, need, st));
+#else
+    VX_CUDA(cudaMemsetAsync(counter, 0, 512, st));  // run cursors
+#endif
     const size_t smem = (size_t)T * (sizeof(K) + (KV ? sizeof(V) : 0));
     const bool vec = ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(vin)) & 15) == 0;
     auto* ds = reinterpret_cast<unsigned long long*>(d_split);
@@ -574,7 +590,7 @@ int vx_profile_read(int64_t* launches, double* ms, uint64_t* elems, int nclass) 
 size_t vx_partition_workspace_bytes(int dtype, int64_t n) {
     (void)dtype;
     const uint64_t T = kPartMinTile;
-    return align_up(((uint64_t)n + T - 1) / T * 8) + 256;
+    return align_up(((uint64_t)n + T - 1) / T * 8) + 512;
 }
 
 int vx_partition(int dtype, const void* in_keys, const void* in_values, void* out_keys, void* out_values, int64_t n,
