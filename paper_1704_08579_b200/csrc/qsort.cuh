@@ -42,7 +42,10 @@ constexpr int kMaxBkt = 2 * kMaxSplit + 1;     // 511 buckets
 #define VX_QS_NT 512
 #endif
 constexpr int kQsNT = VX_QS_NT;                // tile-kernel threads (tile = kQsNT * 8)
-constexpr int kQsMinBlocks = 1024 / kQsNT;
+#ifndef VX_QS_SM_THREADS
+#define VX_QS_SM_THREADS 1024
+#endif
+constexpr int kQsMinBlocks = VX_QS_SM_THREADS / kQsNT;  // resident tile-kernel threads per SM (register cap)
 constexpr int kPlanNT = 512;                   // plan / emit threads
 constexpr int kFinNT = 512;                    // finish-kernel threads
 constexpr int kMaxSample = 4096;
