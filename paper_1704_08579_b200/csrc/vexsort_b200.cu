@@ -305,21 +305,21 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
                 scr_v, lvl_seed, leaf);
         }
         VX_LAUNCHED();
-        // next level's queue sizes, error flags and element counters -> host
-        VX_CUDA(cudaMemcpyAsync(hp, &ctl[level + 1].nseg, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaMemcpyAsync(hp + 1, &c->err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaMemcpyAsync(hp + 2, &c->scat_elems, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        VX_CUDA(cudaMemcpyAsync(hp + 5, &ctl[level + 1].fin_ctr, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        // this level's error flag and element counters and the next level's
+        // queue sizes -> host: the two adjacent Ctl records in one copy
+        static_assert(2 * sizeof(Ctl) <= 256, "pinned scratch holds two Ctl records");
+        Ctl* hc = reinterpret_cast<Ctl*>(hp);
+        VX_CUDA(cudaMemcpyAsync(hc, c, 2 * sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         VX_CUDA(cudaStreamSynchronize(st));
         if (g_prof.on) {
-            prof_elems(KC_SCATTER, hp[2]);
-            prof_elems(KC_FINISH, hp[3]);
-            prof_elems(KC_LOCAL, hp[4]);
+            prof_elems(KC_SCATTER, hc[0].scat_elems);
+            prof_elems(KC_FINISH, hc[0].fin_elems);
+            prof_elems(KC_LOCAL, hc[0].loc_elems);
             prof_collect();
         }
-        if ((unsigned)hp[1]) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
-        nseg = (unsigned)hp[0];
-        if (nseg == 0 && (unsigned)hp[5] == 0) return VX_OK;
+        if (hc[0].err) return fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
+        nseg = hc[1].nseg;
+        if (nseg == 0 && hc[1].fin_ctr == 0) return VX_OK;
     }
     return fail(VX_ECAPACITY, "sort exceeded the maximum level count");
 }
