@@ -351,6 +351,9 @@ __device__ __forceinline__ void cta_bitonic(K* a, V* av, unsigned P) {
     }
 }
 
+#ifndef VX_PLAN_MERGE
+#define VX_PLAN_MERGE 1
+#endif
 // Sort S (pow2, 256..4096) samples in shared memory with the CTA: each warp
 // sorts a 256-sample chunk in registers (the warp bitonic network), then
 // every sample's global rank is its position in its chunk plus its
@@ -373,6 +376,52 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
     }
     __syncthreads();
     if (W == 1) return;
+#if VX_PLAN_MERGE
+    // pairwise merges of sorted runs (256 -> 512 -> ... -> S), in place: each
+    // sample's merged position is its index in its run plus its rank in the
+    // partner run (lower run first on ties: count(< v) for a lower-run
+    // sample, count(<= v) for an upper-run one), found by a fixed-step search
+    // -- log2(run) steps per sample per round instead of 8 per other chunk
+    constexpr unsigned PER = kMaxSample / kPlanNT;
+    const unsigned per = (S + kPlanNT - 1) / kPlanNT;  // samples this thread really moves
+    for (unsigned run = C; run < S; run *= 2) {
+        K val[PER];
+        unsigned dst[PER], lo[PER];
+        const K* oth[PER];
+        bool up[PER];
+#pragma unroll
+        for (unsigned q = 0; q < PER; ++q) {
+            const unsigned i = min(q * kPlanNT + threadIdx.x, S - 1);
+            const unsigned base = i & ~(2 * run - 1);
+            up[q] = (i & run) != 0;
+            val[q] = s[i];
+            oth[q] = s + base + (up[q] ? 0u : run);
+            dst[q] = base + (i & (run - 1));
+            lo[q] = 0;
+        }
+        for (unsigned step = run / 2; step > 0; step >>= 1) {
+#pragma unroll
+            for (unsigned q = 0; q < PER; ++q) {
+                if (q >= per) break;
+                const K e = oth[q][lo[q] + step - 1];
+                const bool before = up[q] ? !(val[q] < e) : (e < val[q]);
+                lo[q] += before ? step : 0u;
+            }
+        }
+#pragma unroll
+        for (unsigned q = 0; q < PER; ++q) {
+            if (q >= per) break;
+            const K e = oth[q][lo[q]];  // lo <= run - 1 here
+            const bool before = up[q] ? !(val[q] < e) : (e < val[q]);
+            dst[q] += lo[q] + (before ? 1u : 0u);
+        }
+        __syncthreads();
+#pragma unroll
+        for (unsigned q = 0; q < PER; ++q)
+            if (q * kPlanNT + threadIdx.x < S) s[dst[q]] = val[q];
+        __syncthreads();
+    }
+#else
     // every thread ranks its PER samples in lockstep: fixed-step branch-free
     // searches, PER independent shared loads per step (the CTA is alone on
     // its SM at level 0, so latency is hidden by ILP, not by other warps)
@@ -416,6 +465,7 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
     for (unsigned q = 0; q < PER; ++q)
         if (q * kPlanNT + threadIdx.x < S) s[rk[q]] = val[q];
     __syncthreads();
+#endif
 }
 
 // ------------------------------------------------------------ init
