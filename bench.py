@@ -152,7 +152,11 @@ def dist_setup(n_gpus):
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        import datetime
+
+        # a hung peer fails the run within minutes instead of blocking forever
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
+                                timeout=datetime.timedelta(seconds=int(os.environ.get("VX_PG_TIMEOUT", "600"))))
     return rank, world, local
 
 
@@ -211,38 +215,35 @@ def ncu_traffic(workload, kernel_class):
 
 
 # ----------------------------------------------------------- our workloads
-def run_ours(args, spec, rank, world, local):
+def make_step(spec, vx, L, dev, rank, world, seed):
+    """Inputs resident in HBM and the step closure (stream-ordered: no host
+    synchronisation inside a step).  Returns a dict with the pieces the
+    verification gate needs."""
     import numpy as np
     import torch
 
-    import paper_1704_08579_b200 as vx
-    from paper_1704_08579_b200 import _lib
-
-    L = _lib.lib()
-    dev = torch.device("cuda", local)
     tdt = torch.int32 if spec["dtype"] == "i32" else torch.float64
     dcode = 0 if spec["dtype"] == "i32" else 1
     esz = 4 if dcode == 0 else 8
-    seed = 1
     kind = spec["kind"]
-
-    # ---------------------------------------------------------- inputs
+    w = {"kind": kind, "esz": esz, "dcode": dcode}
     if kind == "sharded":
         n = spec["n"]
         lo, hi = n * rank // world, n * (rank + 1) // world
         src = torch.empty(hi - lo, dtype=tdt, device=dev)
         gen(L, dcode, DIST[spec["dist"]], src, seed, lo, n)
-        units = n
-        unit_bytes = 2 * esz
-        step = lambda: vx.sharded_sort(src, seed=seed)  # noqa: E731
+        if world == 1:
+            out = torch.empty_like(src)
+            w["step"] = lambda: vx.sort_into(src, out, check=False)  # noqa: E731
+        else:
+            w["step"] = lambda: vx.sharded_sort(src, seed=seed)  # noqa: E731
+        w.update(src=src, units=n, unit_bytes=2 * esz)
     elif kind == "sort":
         n = spec["n"]
         src = torch.empty(n, dtype=tdt, device=dev)
         gen(L, dcode, DIST[spec["dist"]], src, seed, 0, n)
         out = torch.empty_like(src)
-        units = n * world
-        unit_bytes = 2 * esz
-        step = lambda: vx.sort_into(src, out)  # noqa: E731
+        w.update(src=src, units=n * world, unit_bytes=2 * esz, step=lambda: vx.sort_into(src, out, check=False))
     elif kind == "kv":
         n = spec["n"]
         src = torch.empty(n, dtype=tdt, device=dev)
@@ -250,18 +251,22 @@ def run_ours(args, spec, rank, world, local):
         gen(L, dcode, DIST["u31"], src, seed, 0, n)
         gen(L, dcode, DIST["index"], vals, seed, 0, n)
         out, outv = torch.empty_like(src), torch.empty_like(vals)
-        units = n * world
-        unit_bytes = 2 * 2 * esz
-        step = lambda: vx.sort_into(src, out, values=vals, out_values=outv)  # noqa: E731
+        w.update(src=src, vals=vals, units=n * world, unit_bytes=2 * 2 * esz,
+                 step=lambda: (vx.sort_into(src, out, values=vals, out_values=outv, check=False), outv)[0])
+        w["outv"] = outv
     elif kind == "partition":
         n = spec["n"]
         src = torch.empty(n, dtype=tdt, device=dev)
         gen(L, dcode, DIST["normal"], src, seed, 0, n)
         pivot = float(src[vx.select_pivot(src, 0, n - 1)].item())
         out = torch.empty_like(src)
-        units = n * world
-        unit_bytes = 2 * esz
-        step = lambda: vx.partition_region(src, pivot, out=out)  # noqa: E731
+        split = {}
+
+        def pstep():
+            split["b"] = vx.partition_region(src, pivot, out=out)
+            return out
+
+        w.update(src=src, units=n * world, unit_bytes=2 * esz, step=pstep, pivot=pivot, split=split)
     elif kind == "segments":
         import inputs
 
@@ -269,10 +274,73 @@ def run_ours(args, spec, rank, world, local):
         offs_np, vals_np = inputs.c2_input(np.int32 if dcode == 0 else np.float64, nseg=nseg)
         offs = torch.from_numpy(offs_np).to(dev)
         src = torch.from_numpy(vals_np).to(dev)
-        n = len(vals_np)
-        units = n * world
-        unit_bytes = 2 * esz  # + 8 B per offset, added below
-        step = lambda: vx.sort_segments(src, offs, validate=False)  # noqa: E731
+        w.update(src=src, orig=src.clone(), offs=offs, offs_np=offs_np, units=len(vals_np) * world,
+                 unit_bytes=2 * esz, step=lambda: (vx.sort_segments(src, offs, validate=False), src)[1])
+    return w
+
+
+def verify_output(w, out, vx, world):
+    """The correctness gate (benchcli.py:398-427: output == np.sort(input),
+    exit 1 otherwise), as size-independent device checks: ascending order plus
+    an order-independent multiset digest against the input (pairs hashed
+    together); across ranks, boundary order and the global multiset.
+    Raises AssertionError on a mismatch."""
+    import torch
+    import torch.distributed as dist
+    from paper_1704_08579_b200.verify import MASK64, digest, verify_sorted_permutation
+
+    kind = w["kind"]
+    if kind in ("sort", "kv") or (kind == "sharded" and world == 1):
+        verify_sorted_permutation(w["src"], out, w.get("vals"), w.get("outv"))
+        return "sorted + multiset digest == input" + (" (key/value pairs)" if kind == "kv" else "")
+    if kind == "partition":
+        b, p = w["split"]["b"], w["pivot"]
+        assert b == int((w["src"] <= p).sum().item()), "split != count(x <= pivot)"
+        assert bool((out[:b] <= p).all()) and bool((out[b:] > p).all()), "sides violate the pivot"
+        assert digest(w["src"], order=False).multiset() == digest(out, order=False).multiset()
+        return "split == count(<= pivot), sides respect the pivot, multiset digest == input"
+    if kind == "segments":
+        d_in = digest(w["orig"], order=False)
+        d_out = digest(out, order=True, offsets=w["offs"])
+        assert d_out.inversions == 0, f"{d_out.inversions} inversions inside segments"
+        assert d_in.multiset() == d_out.multiset(), "output is not a permutation of the input"
+        return "every segment ascending, multiset digest == input"
+    # sharded over P ranks
+    d_in = digest(w["src"], order=False)
+    d_out = digest(out, order=True)
+    assert d_out.inversions == 0, f"rank-local output not sorted ({d_out.inversions} inversions)"
+    dt = out.dtype
+    edge = torch.zeros(2, dtype=dt, device=out.device)
+    if len(out):
+        edge[0], edge[1] = out[0], out[-1]
+    info = [None] * world
+    dist.all_gather_object(info, {"in": (d_in.n, d_in.hsum, d_in.hxor), "out": (d_out.n, d_out.hsum, d_out.hxor),
+                                  "edge": edge.cpu().tolist() if len(out) else None})
+    tin = [0, 0, 0]
+    tout = [0, 0, 0]
+    last = None
+    for r in info:
+        tin = [tin[0] + r["in"][0], (tin[1] + r["in"][1]) & MASK64, tin[2] ^ r["in"][2]]
+        tout = [tout[0] + r["out"][0], (tout[1] + r["out"][1]) & MASK64, tout[2] ^ r["out"][2]]
+        if r["edge"] is not None:
+            assert last is None or not (r["edge"][0] < last), "rank boundaries out of order"
+            last = r["edge"][1]
+    assert tin == tout, "global output is not a permutation of the global input"
+    return f"rank-local sorted, rank boundaries ordered, global multiset digest == input over {world} ranks"
+
+
+def run_ours(args, spec, rank, world, local):
+    import torch
+
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200 import _lib
+
+    L = _lib.lib()
+    dev = torch.device("cuda", local)
+    seed = 1
+    kind = spec["kind"]
+    w = make_step(spec, vx, L, dev, rank, world, seed)
+    step, units, unit_bytes, src, esz = w["step"], w["units"], w["unit_bytes"], w["src"], w["esz"]
     torch.cuda.synchronize()
 
     # ---------------------------------------------------------- warm-up
@@ -283,9 +351,9 @@ def run_ours(args, spec, rank, world, local):
     barrier()
 
     # ---------------------------------------------------------- timed
+    # the product path: stream-ordered steps (sorts as CUDA graphs), no host
+    # synchronisation inside the region
     stream = torch.cuda.current_stream()
-    L.vx_profile_reset()
-    L.vx_profile_enable(1)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -297,48 +365,102 @@ def run_ours(args, spec, rank, world, local):
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
-    L.vx_profile_enable(0)
     ms = ev0.elapsed_time(ev1)
     ms_max = allmax(ms)
-    launches, kms, kel = prof_read(L)
     value = units * args.steps / (ms_max / 1e3) / 1e9
+
+    # ------------------------------------- one more step: gate + launch count
+    stats = {}
+    if kind in ("sort", "kv") or (kind == "sharded" and world == 1):
+        # rerun the step synchronously with its device counters
+        if kind == "kv":
+            out = torch.empty_like(src)
+            w["outv"] = torch.empty_like(w["vals"])
+            vx.sort_into(src, out, values=w["vals"], out_values=w["outv"], stats=stats)
+        else:
+            out = torch.empty_like(src)
+            vx.sort_into(src, out, stats=stats)
+    else:
+        out = step()
+    torch.cuda.synchronize()
+    try:
+        verified = verify_output(w, out, vx, world)
+        ok = True
+    except AssertionError as e:
+        verified, ok = f"FAILED: {e}", False
+    if stats:
+        # init + every level's kernels (counted on the device) + the loop
+        # control kernel of each WHILE iteration
+        per_step = 1 + stats["launches"] + (stats["levels"] // 2)
+        launches_claim = per_step * args.steps
+    else:
+        launches_claim = None
+    del out
+
+    # ---------------------------------------------------------- profiled pass
+    # per-kernel CUDA events need the eager (host-driven) level loop: the same
+    # kernels, timed one by one on their stream
+    psteps = max(1, min(args.steps, args.prof_steps))
+    L.vx_profile_reset()
+    L.vx_profile_enable(1)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(psteps):
+        r = step()
+        del r
+    e1.record(stream)
+    torch.cuda.synchronize()
+    L.vx_profile_enable(0)
+    prof_ms = e0.elapsed_time(e1) / psteps
+    launches, kms, kel = prof_read(L)
+    if launches_claim is None:
+        launches_claim = int(sum(launches) / psteps * args.steps)
 
     # dominant kernel roofline
     peak, peak_src = peaks()
     dom = max(range(len(CLASSES)), key=lambda i: kms[i])
-    per_elem = unit_bytes
-    alg_bytes = per_elem * kel[dom]
+    alg_bytes = unit_bytes * kel[dom]
     if kind == "segments" and CLASSES[dom] == "segsort":
-        alg_bytes = per_elem * n * args.steps + 8 * (len(offs)) * args.steps
+        alg_bytes = unit_bytes * len(src) * psteps + 8 * len(w["offs"]) * psteps
     achieved = alg_bytes / (kms[dom] / 1e3) / 1e9 if kms[dom] > 0 else 0.0
+    traffic = ncu_traffic(args.workload, CLASSES[dom]) if args.n is None else None
+    alg_per_launch = int(alg_bytes / max(launches[dom], 1))
     roof = {"bound": "hbm", "kernel": CLASSES[dom], "achieved": round(achieved, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": ncu_traffic(args.workload, CLASSES[dom]) if args.n is None else None,
-            "peak_source": peak_src,
-            "alg_bytes_per_launch": int(alg_bytes / max(launches[dom], 1)),
-            "avg_launch_ms": round(kms[dom] / max(launches[dom], 1), 4)}
+            "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+            "traffic_over_alg": round(traffic / alg_per_launch, 3) if traffic and alg_per_launch else None,
+            "peak_source": peak_src, "alg_bytes_per_launch": alg_per_launch,
+            "avg_launch_ms": round(kms[dom] / max(launches[dom], 1), 4),
+            "timing": "CUDA events around every launch of the profiled pass (eager level loop, same kernels)"}
     # whole-step roofline: one read+write pass at HBM peak (+ NVLink term)
     step_bytes = unit_bytes * units / world
     t_roof = step_bytes / (peak * 1e9)
     if kind == "sharded" and world > 1:
         t_roof += (units / world * esz * (world - 1) / world) / (NVL_GBS * 1e9)
-    kernels = {CLASSES[i]: {"launches": launches[i], "ms": round(kms[i], 3), "elems": kel[i]}
+    kernels = {CLASSES[i]: {"launches": launches[i], "ms_per_step": round(kms[i] / psteps, 3),
+                            "elems_per_step": kel[i] // psteps}
                for i in range(len(CLASSES)) if launches[i]}
     res = dict(value=value, ms=ms_max / args.steps, roofline=roof, kernels=kernels,
                step_roofline={"t_roof_ms": round(t_roof * 1e3, 4),
                               "frac": round(t_roof * 1e3 / (ms_max / args.steps), 4),
                               "passes_equiv": round((ms_max / args.steps) / (t_roof * 1e3), 2)},
-               gpu_launches=int(sum(launches)), clocks=clk.summary(), units=units)
+               profiled_ms_per_step=round(prof_ms, 3), gpu_launches=launches_claim, clocks=clk.summary(),
+               units=units, verified=ok, verification=verified)
+    if stats:
+        res["sort_stats"] = {k: stats[k] for k in ("levels", "launches", "scatter_elems", "local_elems",
+                                                   "finish_elems")}
+        res["sort_stats"]["scatter_levels_per_key"] = round(stats["scatter_elems"] / max(len(src), 1), 3)
 
     # ---------------------------------------------------------- e2e
     if not args.no_e2e:
         extra = {}
         if kind == "segments":
-            extra["offs_host"] = torch.from_numpy(offs_np).pin_memory()
-        res["e2e"] = run_e2e(args, spec, vx, L, src, vals if kind == "kv" else None, dev, rank, world, units,
-                             extra)
+            extra["offs_host"] = torch.from_numpy(w["offs_np"]).pin_memory()
+            src.copy_(w["orig"])
+        res["e2e"] = run_e2e(args, spec, vx, L, src, w.get("vals"), dev, rank, world, units, extra)
     # ---------------------------------------------------------- cpu baseline
     if rank == 0 and world == 1 and not args.no_cpu:
-        res["cpu_baseline"] = cpu_baseline(spec, args, src=src)
+        res["cpu_baseline"] = cpu_baseline(spec, args, src=src if kind != "segments" else None)
     return res
 
 
@@ -519,6 +641,7 @@ def main():
     ap.add_argument("--n", type=lambda s: int(eval(s, {}, {})), default=None, help="global n (e.g. 2**28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--prof-steps", type=int, default=2, help="steps of the per-kernel profiled pass")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
@@ -542,15 +665,21 @@ def main():
 
     rank, world, local = dist_setup(args.gpus)
     r = run_ours(args, spec, rank, world, local)
-    cfg["parallelism"] = (f"sample sort over {world} rank(s) (NCCL all-to-all)" if spec["kind"] == "sharded"
+    cfg["parallelism"] = ((f"sample sort over {world} ranks (NCCL all-to-all)" if world > 1 else
+                           "single GPU (P=1 sample sort = the local hybrid sort; no exchange)")
+                          if spec["kind"] == "sharded"
                           else ("replicas" if world > 1 else "single GPU"))
     cfg["l2"] = "inputs larger than the 126 MB L2 (no flush needed)" if r["units"] * 4 > (256 << 20) \
         else "input fits in L2; steps re-run on resident data"
     if rank == 0:
         line = {**base, "value": r["value"], "n_gpus": world, "ms_per_step": r["ms"],
                 "data": "synthetic (device counter-hash generator, seed 1)", "config": cfg,
+                "verified": r["verified"], "verification": r["verification"],
                 "roofline": r["roofline"], "step_roofline": r["step_roofline"], "kernels": r["kernels"],
+                "profiled_ms_per_step": r["profiled_ms_per_step"],
                 "gpu_launches": r["gpu_launches"], "clocks": r["clocks"]}
+        if "sort_stats" in r:
+            line["sort_stats"] = r["sort_stats"]
         if "e2e" in r:
             line["e2e"] = r["e2e"]
         if "cpu_baseline" in r:
@@ -560,6 +689,9 @@ def main():
 
     if dist.is_initialized():
         dist.destroy_process_group()
+    if not r["verified"]:
+        print(f"verification failed: {r['verification']}", file=sys.stderr)
+        sys.exit(1)
 
 
 if __name__ == "__main__":

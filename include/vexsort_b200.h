@@ -12,8 +12,9 @@
  *     copies to the B200, runs the kernels and copies back.  These are what
  *     a maintainer binds in place of `_kernels`.
  *  2. vx_* device API -- device pointers, caller-provided workspace, an
- *     explicit cudaStream_t, stream-ordered, no allocation; used by the
- *     PyTorch-facing Python package and by bench.py.
+ *     explicit cudaStream_t, stream-ordered and CUDA-graph capturable, no
+ *     allocation; used by the PyTorch-facing Python package and bench.py.
+ *     Calls run on the CURRENT device, whose memory the pointers must be.
  *
  * Element kinds (lanes.py:50-63, kind_of lanes.py:502-507): VX_I32 = int32
  * keys, VX_F64 = float64 keys.  Key/value values must have the key's element
@@ -81,6 +82,24 @@ int vx_sort(int dtype, void *keys, void *values, int64_t n, const vx_sort_config
 int vx_sort_into(int dtype, const void *in_keys, const void *in_values, void *out_keys, void *out_values,
                  int64_t n, const vx_sort_config *cfg, void *ws, size_t ws_bytes, vx_stream_t stream);
 
+/* Sorts are stream-ordered: vx_sort / vx_sort_into never synchronise.
+ * Without per-launch timing (vx_profile_enable) the level loop runs as a
+ * CUDA graph with a device-side WHILE condition, so both calls may also be
+ * captured into the caller's own CUDA graph.  Errors found on the device
+ * (work-queue capacity, level limit) land in the workspace; vx_sort_status
+ * synchronises `stream`, returns VX_OK or VX_ECAPACITY for the last sort
+ * that used `ws`, and fills `stats` (may be NULL). */
+typedef struct {
+    uint32_t err;             /* device error bits (0 = ok) */
+    uint32_t levels;          /* partition levels run */
+    uint32_t launches;        /* kernels launched by those levels */
+    uint32_t reserved;
+    uint64_t scatter_elems;   /* elements moved by the global scatter passes */
+    uint64_t finish_elems;    /* elements sorted / copied by the finish kernel */
+    uint64_t local_elems;     /* elements sorted by the CTA-local level */
+} vx_sort_stats;
+int vx_sort_status(const void *ws, int64_t n, vx_stream_t stream, vx_sort_stats *stats);
+
 /* Pivot partition, out of place: out[0:split) <= pivot < out[split:n).
  * *pivot points to a HOST scalar of the key type.  The split (= count of
  * keys <= pivot) is written to the DEVICE int64 *d_split.  Replaces
@@ -95,10 +114,11 @@ int vx_partition(int dtype, const void *in_keys, const void *in_values, void *ou
 /* Batched small sort of CSR segments [offs[s], offs[s+1]) in place, every
  * segment <= 256 elements (config 2).  Replaces one _kernels.smallsort_region
  * call per segment (_kernels.py:115-126; sort_small_region,
- * smallsort.py:218-252).  ws >= 4 bytes holds a device error flag that
- * vx_segments_status() reads back (synchronising). */
-int vx_sort_segments(int dtype, void *keys, void *values, const int64_t *d_offsets, int64_t nseg, void *ws,
-                     size_t ws_bytes, vx_stream_t stream);
+ * smallsort.py:218-252).  n is the length of keys (and values): segments
+ * outside [0, n] are flagged, never touched.  ws >= 4 bytes holds a device
+ * error flag that vx_segments_status() reads back (synchronising). */
+int vx_sort_segments(int dtype, void *keys, void *values, int64_t n, const int64_t *d_offsets, int64_t nseg,
+                     void *ws, size_t ws_bytes, vx_stream_t stream);
 int vx_segments_status(void *ws, vx_stream_t stream);
 
 /* Sharded sample sort building blocks (no reference counterpart; BASELINE
@@ -120,10 +140,22 @@ int vx_select_splitters(int dtype, const void *d_sample_keys, const uint64_t *d_
 int vx_generate(int dtype, int dist, void *out, int64_t n, uint64_t seed, uint64_t global_offset,
                 int64_t global_n, vx_stream_t stream);
 
+/* Output verification on the device (the bench's correctness gate, the
+ * size-independent form of benchcli.py:398-427 "equals np.sort").  Writes 4
+ * device uint64 to d_out: [0] sum and [1] xor of a per-element hash of the
+ * key bits (folded with the value bits when values != NULL) -- an
+ * order-independent multiset digest; [2] adjacent inversions k[i+1] < k[i]
+ * (0 when check_order == 0; counted only inside each CSR segment when
+ * d_offsets[nseg+1] is given); [3] an order-dependent positional digest
+ * sum_i mix64(bits(k[i]) ^ mix64(i)).  Stream-ordered. */
+int vx_verify(int dtype, const void *keys, const void *values, int64_t n, int check_order,
+              const int64_t *d_offsets, int64_t nseg, uint64_t *d_out, vx_stream_t stream);
+
 /* Instrumentation.  Kernel launches are always counted per class; with
  * profiling enabled every launch is also bracketed by CUDA events on its
- * stream.  Classes: 0 plan, 1 hist, 2 emit, 3 scatter, 4 finish,
- * 5 partition, 6 segsort, 7 bucket-partition.  vx_profile_read fills up to
+ * stream (sorts then run their level loop eagerly, host-driven).
+ * Classes: 0 plan, 1 hist, 2 emit, 3 scatter, 4 finish, 5 partition,
+ * 6 segsort, 7 bucket-partition, 8 CTA-local level.  vx_profile_read fills up to
  * nclass entries (launch counts, summed device ms, elements processed) and
  * returns the number of classes. */
 int vx_profile_enable(int on);

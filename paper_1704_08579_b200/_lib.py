@@ -12,7 +12,7 @@ import ctypes
 import os
 import threading
 
-__all__ = ["BackendUnavailable", "lib", "check", "lib_path", "VX_I32", "VX_F64", "SortConfigC"]
+__all__ = ["BackendUnavailable", "lib", "check", "lib_path", "VX_I32", "VX_F64", "SortConfigC", "SortStatsC"]
 
 VX_I32, VX_F64 = 0, 1
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -32,6 +32,18 @@ class SortConfigC(ctypes.Structure):
         ("swap_buffered", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
         ("pivot_seed", ctypes.c_uint64),
+    ]
+
+
+class SortStatsC(ctypes.Structure):
+    _fields_ = [
+        ("err", ctypes.c_uint32),
+        ("levels", ctypes.c_uint32),
+        ("launches", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32),
+        ("scatter_elems", ctypes.c_uint64),
+        ("finish_elems", ctypes.c_uint64),
+        ("local_elems", ctypes.c_uint64),
     ]
 
 
@@ -57,12 +69,14 @@ def _declare(L):
                              ctypes.POINTER(ctypes.c_uint64), i32], i32),
         "vx_partition_workspace_bytes": ([i32, i64], sz),
         "vx_partition": ([i32, vp, vp, vp, vp, i64, vp, vp, vp, sz, vp], i32),
-        "vx_sort_segments": ([i32, vp, vp, vp, i64, vp, sz, vp], i32),
+        "vx_sort_segments": ([i32, vp, vp, i64, vp, i64, vp, sz, vp], i32),
+        "vx_sort_status": ([vp, i64, vp, ctypes.POINTER(SortStatsC)], i32),
         "vx_segments_status": ([vp, vp], i32),
         "vx_bucket_partition_workspace_bytes": ([i32, i32], sz),
         "vx_bucket_partition": ([i32, vp, vp, i64, u64, vp, vp, i32, vp, vp, sz, vp], i32),
         "vx_select_splitters": ([i32, vp, vp, i64, i32, vp, vp, vp], i32),
         "vx_generate": ([i32, i32, vp, i64, u64, u64, i64, vp], i32),
+        "vx_verify": ([i32, vp, vp, i64, i32, vp, i64, vp, vp], i32),
         "vx_host_quicksort": ([i32, vp, i64, i64, i64, i32, i32, i32, u64], i32),
         "vx_host_kv_quicksort": ([i32, vp, vp, i64, i64, i64, i32, i32, i32, u64], i32),
         "vx_host_partition": ([i32, vp, i64, i64, vp, i64, i32, i32], i64),

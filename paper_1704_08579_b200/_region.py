@@ -10,7 +10,7 @@ import numpy as np
 
 from .lanes import ElemKind, kind_of, is_device
 
-__all__ = ["check_region", "check_kv", "workspace", "stream_of", "pivot_for", "host_ptr", "dev_ptr"]
+__all__ = ["check_region", "check_kv", "workspace", "stream_of", "pivot_for", "host_ptr", "dev_ptr", "on_device"]
 
 
 def check_region(region) -> ElemKind:
@@ -50,6 +50,14 @@ def workspace(nbytes: int, device):
     import torch
 
     return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def on_device(t):
+    """Make t's GPU the current device for the duration of a C-ABI call (the
+    library runs on the current device; its per-device state follows it)."""
+    import torch
+
+    return torch.cuda.device(t.device)
 
 
 def stream_of(t) -> ctypes.c_void_p:

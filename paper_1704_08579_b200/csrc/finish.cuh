@@ -508,13 +508,14 @@ __global__ void __launch_bounds__(kFinNT, 2) qs_finish_kernel(const Fin* __restr
                                                            Ctl* __restrict__ ctl_next, Fin* __restrict__ fins_next,
                                                            unsigned cap_fin, K* __restrict__ data_k,
                                                            V* __restrict__ data_v, const K* __restrict__ scr_k,
-                                                           const V* __restrict__ scr_v, uint64_t seed,
-                                                           unsigned leaf) {
+                                                           const V* __restrict__ scr_v, uint64_t sort_seed,
+                                                           const Ctl* __restrict__ tot, unsigned leaf) {
     constexpr bool KV = HasVal<V>::value;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     FinSmem<K, V>& sm = *reinterpret_cast<FinSmem<K, V>*>(smem_raw);
     const unsigned nf = ctl->fin_ctr;
     const unsigned wmax = min(leaf, kWarpSortMax);
+    const uint64_t seed = level_seed(sort_seed, tot);
     for (unsigned d = blockIdx.x; d < nf; d += gridDim.x) {
         const Fin f = fins[d];
         if (threadIdx.x == 0) atomicAdd(&ctl->fin_elems, (unsigned long long)f.len);

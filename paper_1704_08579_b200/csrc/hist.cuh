@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     __shared__ __align__(8) uint64_t s_empty[NS];
     __shared__ BulkTile s_meta[NS];
 
+    if (ctl->err) return;  // the plan ran out of pool capacity: the level is void
     const unsigned ntiles = ctl->tile_ctr;
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);

@@ -52,6 +52,7 @@ constexpr int kMaxSample = 4096;
 constexpr int kFinSample = 1024;
 constexpr uint32_t kCopyChunk = 16384;
 constexpr int kMaxLevels = 48;
+constexpr double kQlSlack = 2.0;  // global levels aim CTA-local leaves at <= this x the target
 
 template <typename K>
 #ifndef VX_QS_IPT
@@ -89,6 +90,11 @@ struct Fin {
     unsigned long long start;
     unsigned len, flags;  // bit0: source is the scratch buffer; bit1: copy only
 };
+// Per-level control record.  A sort keeps three in its workspace: the
+// current level's, the next level's (its queue sizes, filled by this level's
+// emit / finish / local kernels) and the running totals; qs_advance_kernel
+// folds a finished level into the totals, clears its record for reuse two
+// levels later and decides whether another level runs (tot.more).
 struct Ctl {
     unsigned nseg;      // segments in this level's queue
     unsigned spl_ctr, bkt_ctr, tile_ctr, fin_ctr;
@@ -97,9 +103,12 @@ struct Ctl {
     unsigned long long fin_elems;   // elements finished (sorted / copied) at this level
     unsigned long long loc_elems;   // elements sorted by the CTA-local level (local.cuh)
     unsigned ql_ctr;                // CTA-local segments queued by this level's emit
-    unsigned pad_;
+    unsigned level;                 // totals: levels completed (level seeds follow it)
+    unsigned more;                  // totals: another level is needed
+    unsigned launches;              // totals: kernels launched by the completed levels
 };
-enum : unsigned { kErrCapacity = 1, kErrTooLong = 2 };
+static_assert(sizeof(Ctl) == 64, "Ctl is one 64-byte record");
+enum : unsigned { kErrCapacity = 1, kErrTooLong = 2, kErrLevels = 4, kErrOffsets = 8 };
 
 // ------------------------------------------------------------ classifiers
 // ---------------------------------------------------- cell-table classifier
@@ -469,12 +478,60 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
 }
 
 // ------------------------------------------------------------ init
-__global__ void qs_init_kernel(Seg* segs, Ctl* ctl, unsigned long long n) {
-    segs[0].start = 0;
-    segs[0].len = n;
-    segs[0].lo = 1;
-    segs[0].hi = 0;
-    ctl[0].nseg = 1;
+// Clears the three control records and queues the whole array: one level
+// segment, or (n <= the finish capacity) one finish item whose source is the
+// input (root_flags bit0).
+__global__ void qs_init_kernel(Seg* segs, Ctl* ctl, Fin* fins, unsigned long long n, unsigned as_fin,
+                               unsigned root_flags) {
+    unsigned* w = reinterpret_cast<unsigned*>(ctl);
+    for (unsigned i = threadIdx.x; i < 3 * sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (as_fin) {
+            fins[0].start = 0;
+            fins[0].len = (unsigned)n;
+            fins[0].flags = root_flags;
+            ctl[0].fin_ctr = 1;
+        } else {
+            segs[0].start = 0;
+            segs[0].len = n;
+            segs[0].lo = 1;
+            segs[0].hi = 0;
+            ctl[0].nseg = 1;
+        }
+    }
+}
+
+// Level seed: the sort's seed mixed with the number of completed levels.
+__device__ __forceinline__ uint64_t level_seed(uint64_t seed, const Ctl* tot) {
+    return mix64(seed + 0x51ED270B27AD1CULL * (tot->level + 1));
+}
+
+// After every kernel of a level: fold its record c into the totals, flag a
+// level-count overflow, clear c (it serves as the "next" record two levels
+// on) and decide whether another level is needed.  In a CUDA graph it also
+// sets the level loop's condition (set_cond).
+__global__ void qs_advance_kernel(Ctl* c, const Ctl* nx, Ctl* tot, unsigned kernels,
+                                  cudaGraphConditionalHandle cond, int set_cond) {
+    tot->scat_elems += c->scat_elems;
+    tot->fin_elems += c->fin_elems;
+    tot->loc_elems += c->loc_elems;
+    tot->err |= c->err;
+    tot->launches += kernels + 1;
+    tot->level += 1;
+    unsigned more = (tot->err == 0 && (nx->nseg > 0 || nx->fin_ctr > 0)) ? 1u : 0u;
+    if (more && tot->level >= (unsigned)kMaxLevels) {
+        tot->err |= kErrLevels;
+        more = 0;
+    }
+    tot->more = more;
+    *c = Ctl{};
+    if (set_cond) cudaGraphSetConditional(cond, more);
+}
+
+// Body tail of the graph's level loop: continue while tot.more.
+__global__ void qs_loopctl_kernel(const Ctl* tot, cudaGraphConditionalHandle cond) {
+    cudaGraphSetConditional(cond, tot->more);
 }
 
 // ------------------------------------------------------------ plan
@@ -483,13 +540,14 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                                                           Ctl* __restrict__ ctl, K* __restrict__ spl_pool,
                                                           unsigned long long* __restrict__ bkt_pool,
                                                           unsigned* __restrict__ tile_owner, unsigned cap_spl,
-                                                          unsigned cap_bkt, unsigned cap_tiles, uint64_t seed,
-                                                          uint64_t ql_target) {
+                                                          unsigned cap_bkt, unsigned cap_tiles, uint64_t sort_seed,
+                                                          const Ctl* __restrict__ tot, uint64_t ql_target) {
     constexpr int TILE = qs_tile<K>();
     __shared__ K s_samp[kMaxSample];
     __shared__ unsigned s_scan[kPlanNT / 32 + 1];
     __shared__ unsigned s_off[3];
     const unsigned nseg = ctl->nseg;
+    const uint64_t seed = level_seed(sort_seed, tot);
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const uint64_t start = segs[s].start, len = segs[s].len;
         unsigned mt;
@@ -499,10 +557,15 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             mt = (unsigned)max((uint64_t)2, min((uint64_t)kMaxSplit, mt64));
         } else {
             // aim the leaves of the remaining levels at the CTA-local level's
-            // target, fan-out balanced over them: L = ceil(log_256(r)) levels
-            // of r^(1/L) buckets, r = len / target
+            // target, fan-out balanced over them: L levels of r^(1/L) buckets,
+            // r = len / target.  L counts against TWICE the target
+            // (kQlSlack): the CTA-local level takes up to 3x the target, so
+            // leaves up to 2x (x1.25 sampling spread) still fit.  Counting
+            // against the target itself sent every level-0 bucket even
+            // slightly above 256 x target (half of them at n = 2^32) through
+            // two more levels of fan-out ~17 instead of one of 256.
             const double r = (double)len / (double)ql_target;
-            const double L = ceil(log(r) / log(256.0) - 1e-9);
+            const double L = ceil(log(r / kQlSlack) / log(256.0) - 1e-9);
             const double f = ceil(pow(r, 1.0 / (L < 1.0 ? 1.0 : L)) - 1e-9);
             mt = (unsigned)max(2.0, min((double)kMaxSplit, f - 1.0));
         }
@@ -531,6 +594,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 unsigned bo = atomicAdd(&ctl->bkt_ctr, nb);
                 unsigned to = atomicAdd(&ctl->tile_ctr, ntiles);
                 if (bo + nb > cap_bkt || to + ntiles > cap_tiles) {
+                    // capacity exceeded: flag it; hist / emit / scatter skip the
+                    // level (they test ctl->err), so no pool slot is aliased
                     atomicOr(&ctl->err, kErrCapacity);
                     bo = to = 0;
                 }
@@ -676,6 +741,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
     static_assert(kPlanNT >= kMaxBkt, "one thread per bucket");
     constexpr uint32_t LOCAL = FinCap<K, V>::value;
     __shared__ unsigned long long s_scan[kPlanNT / 32];
+    if (ctl->err) return;  // the plan ran out of pool capacity: the level is void
     const unsigned nseg = ctl->nseg;
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const Seg sg = segs[s];
@@ -822,15 +888,20 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
 
 // ------------------------------------------------------------ segments API
 // Batched bitonic over CSR segments (config 2): one warp per segment,
-// in place, lengths <= 256 (longer segments flag kErrTooLong, untouched).
+// in place, lengths <= 256 (longer segments flag kErrTooLong, untouched;
+// offsets outside [0, n] or decreasing flag kErrOffsets, untouched).
 template <typename K, typename V>
-__global__ void __launch_bounds__(256) segsort_kernel(K* __restrict__ k, V* __restrict__ v,
+__global__ void __launch_bounds__(256) segsort_kernel(K* __restrict__ k, V* __restrict__ v, uint64_t n,
                                                       const long long* __restrict__ offs, uint64_t nseg,
                                                       unsigned* __restrict__ err) {
     const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x >> 5);
     for (uint64_t s = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nseg; s += warps) {
         const long long lo = offs[s], hi = offs[s + 1];
         const long long len = hi - lo;
+        if (lo < 0 || hi < lo || (unsigned long long)hi > n) {
+            if ((threadIdx.x & 31) == 0) atomicOr(err, kErrOffsets);
+            continue;
+        }
         if (len < 2) continue;
         if (len > 256) {
             if ((threadIdx.x & 31) == 0) atomicOr(err, kErrTooLong);
@@ -877,15 +948,13 @@ __global__ void __launch_bounds__(kQsNT) bp_hist_kernel(const K* __restrict__ sr
     }
 }
 
-__global__ void bp_scan_kernel(const unsigned long long* __restrict__ counts, unsigned nb,
-                               unsigned long long* __restrict__ cursor) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        unsigned long long acc = 0;
-        for (unsigned b = 0; b < nb; ++b) {
-            cursor[b] = acc;
-            acc += counts[b];
-        }
-    }
+// destination cursors = exclusive scan of the counts (nb <= 256, one CTA)
+__global__ void __launch_bounds__(256) bp_scan_kernel(const unsigned long long* __restrict__ counts, unsigned nb,
+                                                      unsigned long long* __restrict__ cursor) {
+    __shared__ unsigned long long s_scan[256 / 32];
+    const unsigned long long c = threadIdx.x < nb ? counts[threadIdx.x] : 0ull;
+    const unsigned long long ex = block_excl_scan_u64<256>(c, s_scan);
+    if (threadIdx.x < nb) cursor[threadIdx.x] = ex;
 }
 
 template <typename K, typename V>

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterPipeSmem<K, V>& sm = *reinterpret_cast<ScatterPipeSmem<K, V>*>(smem_raw);
+    if (ctl->err) return;  // the plan ran out of pool capacity: the level is void
     const unsigned ntiles = ctl->tile_ctr;
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);

@@ -14,7 +14,7 @@ from ._lib import check, lib
 from ._region import check_kv, dev_ptr, host_ptr, pivot_for, stream_of, workspace
 from .lanes import get_backend, is_device
 from .partition import _device_partition
-from .quicksort import MAX_PACKS, SortConfig, _PIVOT_STRATEGIES, _U64, _cfg, _resolve_bound
+from .quicksort import MAX_PACKS, SortConfig, _PIVOT_STRATEGIES, _U64, _device_sort, _resolve_bound
 
 __all__ = ["kv_sort", "sort_kv", "kv_partition_region", "kv_sort_small_region", "kv_scalar_partition"]
 
@@ -30,10 +30,7 @@ def kv_sort(keys, values, config: SortConfig | None = None) -> None:
     bound = _resolve_bound(config, backend.lanes)
     L = lib()
     if is_device(keys):
-        ws = workspace(L.vx_sort_workspace_bytes(kind.code, 1, n), keys.device)
-        cfg = _cfg(config, bound)
-        check(L.vx_sort(kind.code, dev_ptr(keys), dev_ptr(values), n, ctypes.byref(cfg), dev_ptr(ws), ws.numel(),
-                        stream_of(keys)), "kv_sort")
+        _device_sort(kind, keys, values, keys, values, config, bound, True, "kv_sort")
         return
     check(L.vx_host_kv_quicksort(kind.code, host_ptr(keys), host_ptr(values), n, backend.lanes, bound,
                                  _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),

@@ -13,7 +13,7 @@ from __future__ import annotations
 import ctypes
 
 from ._lib import check, lib
-from ._region import check_region, dev_ptr, host_ptr, pivot_for, stream_of, workspace
+from ._region import check_region, dev_ptr, host_ptr, on_device, pivot_for, stream_of, workspace
 from .lanes import get_backend, is_device
 
 __all__ = ["partition_region", "scalar_partition"]
@@ -24,12 +24,13 @@ def _device_partition(kind, keys, values, pivot_c, out_keys, out_values):
 
     n = len(keys)
     L = lib()
-    ws = workspace(L.vx_partition_workspace_bytes(kind.code, n), keys.device)
-    split = torch.empty(1, dtype=torch.int64, device=keys.device)
-    check(L.vx_partition(kind.code, dev_ptr(keys), dev_ptr(values) if values is not None else None,
-                         dev_ptr(out_keys), dev_ptr(out_values) if out_values is not None else None, n,
-                         ctypes.byref(pivot_c), dev_ptr(split), dev_ptr(ws), ws.numel(), stream_of(keys)),
-          "partition")
+    with on_device(keys):
+        ws = workspace(L.vx_partition_workspace_bytes(kind.code, n), keys.device)
+        split = torch.empty(1, dtype=torch.int64, device=keys.device)
+        check(L.vx_partition(kind.code, dev_ptr(keys), dev_ptr(values) if values is not None else None,
+                             dev_ptr(out_keys), dev_ptr(out_values) if out_values is not None else None, n,
+                             ctypes.byref(pivot_c), dev_ptr(split), dev_ptr(ws), ws.numel(), stream_of(keys)),
+              "partition")
     return split
 
 

@@ -12,8 +12,8 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
-from ._lib import SortConfigC, check, lib
-from ._region import check_region, dev_ptr, host_ptr, stream_of, workspace
+from ._lib import SortConfigC, SortStatsC, check, lib
+from ._region import check_kv, check_region, dev_ptr, host_ptr, on_device, stream_of, workspace
 from .lanes import get_backend, is_device
 
 __all__ = ["SortConfig", "sort", "sort_with_config", "sort_into", "select_pivot", "MAX_PACKS"]
@@ -87,34 +87,55 @@ def sort_with_config(region, config: SortConfig) -> None:
     bound = _resolve_bound(config, backend.lanes)
     L = lib()
     if is_device(region):
-        ws = workspace(L.vx_sort_workspace_bytes(kind.code, 0, n), region.device)
-        cfg = _cfg(config, bound)
-        check(L.vx_sort(kind.code, dev_ptr(region), None, n, ctypes.byref(cfg), dev_ptr(ws), ws.numel(),
-                        stream_of(region)), "sort")
+        _device_sort(kind, region, None, region, None, config, bound, True, "sort")
         return
     check(L.vx_host_quicksort(kind.code, host_ptr(region), n, backend.lanes, bound,
                               _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),
                               int(config.swap_buffered), int(config.pivot_seed) & _U64), "sort")
 
 
-def sort_into(src, out, config: SortConfig | None = None, values=None, out_values=None):
+def _device_sort(kind, src, values, out, out_values, config, bound, check_status, what, stats=None):
+    """vx_sort_into on src's device and current stream; with check_status the
+    stream is synchronised once at the end and device-side errors raise."""
+    L = lib()
+    n = len(src)
+    with on_device(src):
+        ws = workspace(L.vx_sort_workspace_bytes(kind.code, int(values is not None), n), src.device)
+        cfg = _cfg(config, bound)
+        st = stream_of(src)
+        check(L.vx_sort_into(kind.code, dev_ptr(src), dev_ptr(values) if values is not None else None,
+                             dev_ptr(out), dev_ptr(out_values) if out_values is not None else None, n,
+                             ctypes.byref(cfg), dev_ptr(ws), ws.numel(), st), what)
+        if check_status or stats is not None:
+            s = SortStatsC()
+            check(L.vx_sort_status(dev_ptr(ws), n, st, ctypes.byref(s)), what)
+            if stats is not None:
+                stats.update({f: getattr(s, f) for f, _ in SortStatsC._fields_ if f != "reserved"})
+    return out
+
+
+def sort_into(src, out, config: SortConfig | None = None, values=None, out_values=None, *, check: bool = True,
+              stats: dict | None = None):
     """Device-only out-of-place sort: out = sorted(src) (pairs with values /
     out_values).  src is only read, by the first partition level, so this
-    costs the same HBM traffic as the in-place sort."""
+    costs the same HBM traffic as the in-place sort.  check=False keeps the
+    call fully stream-ordered (no synchronisation; capturable into a CUDA
+    graph) and skips the device error check; `stats` (a dict) receives the
+    level / launch counters of the sort (synchronises)."""
     config = config or SortConfig()
     kind = check_region(src)
-    assert is_device(src) and is_device(out) and out.dtype == src.dtype and len(out) == len(src)
-    assert out.is_contiguous()
-    n = len(src)
+    assert is_device(src) and is_device(out), "sort_into takes CUDA tensors"
+    check_region(out)
+    assert out.dtype == src.dtype and len(out) == len(src) and out.device == src.device
+    assert (values is None) == (out_values is None), "values and out_values go together"
+    if values is not None:
+        check_kv(src, values)
+        check_kv(out, out_values)
     backend = get_backend(config.backend, kind)
     bound = _resolve_bound(config, backend.lanes)
-    L = lib()
-    ws = workspace(L.vx_sort_workspace_bytes(kind.code, int(values is not None), n), src.device)
-    cfg = _cfg(config, bound)
-    check(L.vx_sort_into(kind.code, dev_ptr(src), dev_ptr(values) if values is not None else None, dev_ptr(out),
-                         dev_ptr(out_values) if out_values is not None else None, n, ctypes.byref(cfg),
-                         dev_ptr(ws), ws.numel(), stream_of(src)), "sort_into")
-    return out
+    if len(src) == 0:
+        return out
+    return _device_sort(kind, src, values, out, out_values, config, bound, check, "sort_into", stats)
 
 
 def sort(region, config: SortConfig | None = None) -> None:

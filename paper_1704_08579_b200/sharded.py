@@ -27,7 +27,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 from ._lib import check, lib
-from ._region import check_region, dev_ptr, stream_of, workspace
+from ._region import check_region, dev_ptr, on_device, stream_of, workspace
 from .quicksort import SortConfig, sort_into, sort_with_config
 
 __all__ = ["sharded_sort", "sample_positions", "B200Ops", "ExchangeStats"]
@@ -64,10 +64,11 @@ class B200Ops:
 
         kind = check_region(keys)
         m = nparts - 1
-        sk = torch.empty(max(m, 1), dtype=keys.dtype, device=keys.device)
-        si = torch.empty(max(m, 1), dtype=torch.int64, device=keys.device)
-        check(lib().vx_select_splitters(kind.code, dev_ptr(keys), dev_ptr(gidx), len(keys), nparts, dev_ptr(sk),
-                                        dev_ptr(si), stream_of(keys)), "select_splitters")
+        with on_device(keys):
+            sk = torch.empty(max(m, 1), dtype=keys.dtype, device=keys.device)
+            si = torch.empty(max(m, 1), dtype=torch.int64, device=keys.device)
+            check(lib().vx_select_splitters(kind.code, dev_ptr(keys), dev_ptr(gidx), len(keys), nparts, dev_ptr(sk),
+                                            dev_ptr(si), stream_of(keys)), "select_splitters")
         return sk[:m], si[:m]
 
     def bucket_partition(self, local, gofs, sk, si):
@@ -75,13 +76,14 @@ class B200Ops:
 
         kind = check_region(local)
         m = len(sk)
-        out = torch.empty_like(local)
-        counts = torch.empty(m + 1, dtype=torch.int64, device=local.device)
-        L = lib()
-        ws = workspace(L.vx_bucket_partition_workspace_bytes(kind.code, m), local.device)
-        check(L.vx_bucket_partition(kind.code, dev_ptr(local), dev_ptr(out), len(local), int(gofs),
-                                    dev_ptr(sk) if m else None, dev_ptr(si) if m else None, m, dev_ptr(counts),
-                                    dev_ptr(ws), ws.numel(), stream_of(local)), "bucket_partition")
+        with on_device(local):
+            out = torch.empty_like(local)
+            counts = torch.empty(m + 1, dtype=torch.int64, device=local.device)
+            L = lib()
+            ws = workspace(L.vx_bucket_partition_workspace_bytes(kind.code, m), local.device)
+            check(L.vx_bucket_partition(kind.code, dev_ptr(local), dev_ptr(out), len(local), int(gofs),
+                                        dev_ptr(sk) if m else None, dev_ptr(si) if m else None, m, dev_ptr(counts),
+                                        dev_ptr(ws), ws.numel(), stream_of(local)), "bucket_partition")
         return out, counts
 
     def local_sort(self, x, seed):
@@ -94,11 +96,50 @@ class B200Ops:
         return sort_into(x, torch.empty_like(x), SortConfig(pivot_seed=seed))
 
 
+class _Comm:
+    """The collectives of the exchange on `group`.  NCCL moves CUDA tensors
+    directly (NVLink / NVSwitch); other backends (gloo: CPU tests, one-GPU
+    multi-process tests) get host-staged copies."""
+
+    def __init__(self, group, dev):
+        import torch.distributed as dist
+
+        self.group = group
+        self.dev = dev
+        self.staged = dev.type == "cuda" and dist.get_backend(group) != "nccl"
+
+    def _h(self, t):
+        return t.cpu() if self.staged else t
+
+    def _d(self, t):
+        return t.to(self.dev) if self.staged else t
+
+    def all_gather(self, t):
+        import torch
+        import torch.distributed as dist
+
+        P = dist.get_world_size(self.group)
+        src = self._h(t)
+        out = torch.empty(P * len(src), dtype=src.dtype, device=src.device)
+        dist.all_gather_into_tensor(out, src, group=self.group)
+        return self._d(out)
+
+    def all_to_all(self, out_len, x, send, recv):
+        import torch
+        import torch.distributed as dist
+
+        src = self._h(x)
+        out = torch.empty(out_len, dtype=src.dtype, device=src.device)
+        dist.all_to_all_single(out, src, output_split_sizes=recv, input_split_sizes=send, group=self.group)
+        return self._d(out)
+
+
 def sharded_sort(local, group=None, *, samples_per_rank: int = 1024, seed: int = 0, ops=None,
                  stats: ExchangeStats | None = None):
     """Globally sort the distributed array whose shard on this rank is
     `local` (1-D, contiguous; global order = rank order).  Returns this
-    rank's slice of the sorted result (a new tensor; size varies by rank)."""
+    rank's slice of the sorted result (a new tensor; size varies by rank).
+    Raises RuntimeError if the exchange loses or duplicates elements."""
     import torch
     import torch.distributed as dist
 
@@ -115,13 +156,18 @@ def sharded_sort(local, group=None, *, samples_per_rank: int = 1024, seed: int =
             stats.send_counts = stats.recv_counts = [n_local]
         return out
     dev = local.device
+    comm = _Comm(group, dev)
     # global offset of this shard
-    sizes = torch.zeros(P, dtype=torch.int64, device=dev)
-    mine = torch.tensor([n_local], dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(sizes, mine, group=group)
-    gofs = int(sizes[:r].sum().item())
-    # samples with global indices; fixed count per rank (pad with the last
-    # element of the shard, or a sentinel-free empty marker when empty)
+    sizes = comm.all_gather(torch.tensor([n_local], dtype=torch.int64, device=dev)).tolist()
+    gofs = int(sum(sizes[:r]))
+    n_total = int(sum(sizes))
+    if n_total == 0:
+        if stats is not None:
+            stats.n_local_out = 0
+            stats.send_counts = stats.recv_counts = [0] * P
+        return local.clone()
+    # samples with global indices; fixed count per rank (padded; the valid
+    # count travels with them)
     s = max(1, min(samples_per_rank, 8192 // P))
     pos = sample_positions(n_local, s, r, seed).to(dev)
     cnt = torch.tensor([len(pos)], dtype=torch.int64, device=dev)
@@ -130,21 +176,25 @@ def sharded_sort(local, group=None, *, samples_per_rank: int = 1024, seed: int =
     if len(pos):
         skeys[: len(pos)] = local[pos]
         sidx[: len(pos)] = pos + gofs
-    all_keys = torch.empty(P * s, dtype=local.dtype, device=dev)
-    all_idx = torch.empty(P * s, dtype=torch.int64, device=dev)
-    all_cnt = torch.empty(P, dtype=torch.int64, device=dev)
-    dist.all_gather_into_tensor(all_keys, skeys, group=group)
-    dist.all_gather_into_tensor(all_idx, sidx, group=group)
-    dist.all_gather_into_tensor(all_cnt, cnt, group=group)
+    all_keys = comm.all_gather(skeys)
+    all_idx = comm.all_gather(sidx)
+    all_cnt = comm.all_gather(cnt)
     valid = torch.cat([torch.arange(r_ * s, r_ * s + int(c), device=dev) for r_, c in enumerate(all_cnt.tolist())])
     sk, si = ops.select_splitters(all_keys[valid].contiguous(), all_idx[valid].contiguous(), P)
     parted, counts = ops.bucket_partition(local, gofs, sk, si)
-    recv_counts = torch.empty_like(counts)
-    dist.all_to_all_single(recv_counts, counts, group=group)
     send = counts.tolist()
-    recv = recv_counts.tolist()
-    out = torch.empty(int(sum(recv)), dtype=local.dtype, device=dev)
-    dist.all_to_all_single(out, parted, output_split_sizes=recv, input_split_sizes=send, group=group)
+    # counts matrix: row q = what rank q sends to each rank
+    cmat = comm.all_gather(counts).view(P, P).tolist()
+    recv = [cmat[q][r] for q in range(P)]
+    if sum(send) != n_local:
+        raise RuntimeError(f"bucket partition lost elements on rank {r}: {sum(send)} != {n_local}")
+    out = comm.all_to_all(int(sum(recv)), parted, send, recv)
+    # post-exchange check: the global count is conserved and every rank got
+    # what the counts matrix says
+    got = comm.all_gather(torch.tensor([len(out)], dtype=torch.int64, device=dev)).tolist()
+    want = [sum(cmat[q][d] for q in range(P)) for d in range(P)]
+    if got != want or sum(got) != n_total:
+        raise RuntimeError(f"exchange count mismatch: received {got}, expected {want} (total {n_total})")
     out = ops.local_sort(out, seed)
     if stats is not None:
         stats.n_local_out = len(out)

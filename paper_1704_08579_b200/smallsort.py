@@ -11,7 +11,7 @@ network per segment in a single launch (csrc/bitonic.cuh).
 from __future__ import annotations
 
 from ._lib import check, lib
-from ._region import check_region, dev_ptr, host_ptr, stream_of, workspace
+from ._region import check_region, dev_ptr, host_ptr, on_device, stream_of, workspace
 from .lanes import ElemKind, get_backend, is_device
 from .quicksort import MAX_PACKS, SortConfig, sort_with_config
 
@@ -44,7 +44,8 @@ def sort_segments(values, offsets, payload=None, *, validate: bool = True) -> No
     place (device tensors; offsets int64 of length nseg+1).  With `payload`
     (same length and element width), pairs move together and are swapped only
     on strict key inversion, as in the reference's kv network.  validate=True
-    synchronises and raises AssertionError if a segment exceeds 256."""
+    synchronises and raises AssertionError if a segment exceeds 256 or an
+    offset lies outside [0, len(values)] (such segments are never touched)."""
     import torch
 
     kind = check_region(values)
@@ -58,9 +59,10 @@ def sort_segments(values, offsets, payload=None, *, validate: bool = True) -> No
     if nseg <= 0:
         return
     L = lib()
-    ws = workspace(256, values.device)
-    st = stream_of(values)
-    check(L.vx_sort_segments(kind.code, dev_ptr(values), dev_ptr(payload) if payload is not None else None,
-                             dev_ptr(offsets), nseg, dev_ptr(ws), ws.numel(), st), "sort_segments")
-    if validate:
-        check(L.vx_segments_status(dev_ptr(ws), st), "sort_segments")
+    with on_device(values):
+        ws = workspace(256, values.device)
+        st = stream_of(values)
+        check(L.vx_sort_segments(kind.code, dev_ptr(values), dev_ptr(payload) if payload is not None else None,
+                                 len(values), dev_ptr(offsets), nseg, dev_ptr(ws), ws.numel(), st), "sort_segments")
+        if validate:
+            check(L.vx_segments_status(dev_ptr(ws), st), "sort_segments")

@@ -1,0 +1,201 @@
+"""Full-size parity (BASELINE configs 2 and 5 at their benchmarked sizes),
+the stream-ordered / CUDA-graph contract of the sort, and API validation.
+
+* C5: int32 n = 2^32 and float64 n = 2^31 under the four distributions,
+  generated on the device exactly as bench.py does.  The output must
+  reproduce the positional digest of ``np.sort`` of the same input
+  (tests/golden/full_digests.json, made by make_full_digests.py from a numpy
+  replica of the generator, itself pinned below), be ascending, and hold the
+  input's multiset.  np.sort is the reference's oracle for a full sort
+  (pkg/src/vexsort/oracle.py:15-21).
+* C2: all 2^20 CSR segments against the digest of the REFERENCE's own
+  per-segment small sort (smallsort.py:218-252 / _kernels.py:115-126).
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _full():
+    with open(os.path.join(HERE, "golden", "full_digests.json")) as f:
+        return json.load(f)
+
+
+def _free():
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("tdt", [torch.int32, torch.float64])
+@pytest.mark.parametrize("dist", ["uniform", "sorted", "reverse", "few"])
+def test_generator_matches_numpy_replica(tdt, dist):
+    """The device generator is what the full-size digests were computed from."""
+    from make_full_digests import gen_numpy
+
+    from paper_1704_08579_b200.verify import generate
+
+    gn = 1 << 32 if tdt == torch.int32 else 1 << 31
+    for g0 in (0, gn - (1 << 16), 12345 << 10):
+        t = generate(tdt, dist, 1 << 16, global_offset=g0, global_n=gn)
+        want = gen_numpy(tdt == torch.int32, dist, g0, 1 << 16, gn)
+        assert np.array_equal(t.cpu().numpy().view(np.uint8), want.view(np.uint8)), (dist, g0)
+
+
+@pytest.mark.parametrize("tag,tdt,n", [("i32", torch.int32, 1 << 32), ("f64", torch.float64, 1 << 31)])
+@pytest.mark.parametrize("dist", ["uniform", "sorted", "reverse", "few"])
+def test_c5_full_size_matches_oracle(tag, tdt, n, dist):
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200.verify import digest, generate
+
+    gold = _full().get(f"c5_{tag}_{dist}")
+    assert gold is not None, "run tests/golden/make_full_digests.py c5"
+    _free()
+    src = generate(tdt, dist, n)
+    d_in = digest(src, order=False)
+    assert (d_in.hsum, d_in.hxor) == (gold["hsum"], gold["hxor"]), "device input differs from the digest's input"
+    out = torch.empty_like(src)
+    stats = {}
+    vx.sort_into(src, out, stats=stats)
+    d_out = digest(out, order=True)
+    assert d_out.inversions == 0
+    assert d_out.multiset() == d_in.multiset()
+    assert d_out.positional == gold["sorted_positional"], "output differs from np.sort(input)"
+    assert out[0].item() == gold["first"] and out[-1].item() == gold["last"]
+    if dist == "uniform":
+        # two global partition levels, then the CTA-local level: every key is
+        # moved by exactly two scatter passes (no spurious third level)
+        assert stats["scatter_elems"] <= 2 * n, stats
+        assert stats["local_elems"] >= 0.95 * n, stats
+    if dist in ("sorted", "reverse"):
+        # the exact answer is known: the sorted generator itself
+        want = generate(tdt, "sorted", n)
+        assert torch.equal(out, want)
+        del want
+    del src, out
+    _free()
+
+
+@pytest.mark.parametrize("tag,dt", [("i32", np.int32), ("f64", np.float64)])
+def test_c2_full_size_matches_reference_digest(tag, dt):
+    """All 2^20 segments (grid-stride loop of the segment kernel repeats)."""
+    import inputs
+
+    import paper_1704_08579_b200 as vx
+
+    gold = _full()[f"c2_{tag}_2^20seg"]
+    offs, vals = inputs.c2_input(dt, nseg=1 << 20)
+    h = hashlib.blake2b(digest_size=16)
+    h.update(offs.tobytes())
+    h.update(vals.tobytes())
+    assert h.hexdigest() == gold["in"]
+    t = torch.from_numpy(vals).cuda()
+    o = torch.from_numpy(offs).cuda()
+    vx.sort_segments(t, o)
+    h = hashlib.blake2b(digest_size=16)
+    h.update(t.cpu().numpy().tobytes())
+    assert h.hexdigest() == gold["out"]
+
+
+def test_sort_captured_in_cuda_graph():
+    """vx_sort_into is stream-ordered: it records into the caller's capture
+    (the level loop becomes a conditional WHILE node) and replays on new
+    data in the same buffers."""
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200.verify import generate, verify_sorted_permutation
+
+    for tdt, n in ((torch.int32, 1 << 20), (torch.int32, 1 << 24), (torch.float64, 3 << 20), (torch.int32, 5000)):
+        src = generate(tdt, "uniform", n, seed=11)
+        out = torch.empty_like(src)
+        vx.sort_into(src, out)  # warm-up outside the capture (workspace, attributes)
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                vx.sort_into(src, out, check=False)
+        torch.cuda.current_stream().wait_stream(s)
+        for seed in (12, 13):
+            src.copy_(generate(tdt, "uniform", n, seed=seed))
+            out.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            verify_sorted_permutation(src, out)
+        few = generate(tdt, "few", n, seed=5)
+        src.copy_(few)
+        g.replay()
+        torch.cuda.synchronize()
+        verify_sorted_permutation(src, out)
+        del g
+
+
+def test_stream_ordered_sorts_back_to_back():
+    """Many sorts queued without synchronisation, each on its own buffers,
+    then checked: no host round trip is needed between them."""
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200.verify import generate, verify_sorted_permutation
+
+    srcs = [generate(torch.int32, d, 1 << 21, seed=3) for d in ("uniform", "sorted", "reverse", "few")]
+    srcs += [generate(torch.float64, d, 1 << 20, seed=4) for d in ("uniform", "few")]
+    outs = [torch.empty_like(s) for s in srcs]
+    for s, o in zip(srcs, outs):
+        vx.sort_into(s, o, check=False)
+    torch.cuda.synchronize()
+    for s, o in zip(srcs, outs):
+        verify_sorted_permutation(s, o)
+
+
+def test_sort_stats_levels():
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200.verify import generate
+
+    src = generate(torch.int32, "uniform", 1 << 20)
+    st = {}
+    vx.sort_into(src, torch.empty_like(src), stats=st)
+    # one level: partition around <= 255 pivots, then the same level's finish
+    # kernel sorts every bucket (<= 8192 keys) -- one graph, no host round trip
+    assert st["err"] == 0 and st["levels"] == 1 and st["launches"] == 6, st
+    src = generate(torch.int32, "uniform", 4000)
+    st = {}
+    vx.sort_into(src, torch.empty_like(src), stats=st)
+    assert st["levels"] == 1 and st["finish_elems"] == 4000 and st["scatter_elems"] == 0, st
+
+
+def test_sort_into_validates_payloads():
+    import paper_1704_08579_b200 as vx
+
+    k = torch.arange(100, dtype=torch.int32, device="cuda")
+    v = torch.arange(100, dtype=torch.int32, device="cuda")
+    with pytest.raises(AssertionError):
+        vx.sort_into(k, torch.empty_like(k), values=v)  # out_values missing
+    with pytest.raises(AssertionError):
+        vx.sort_into(k, torch.empty_like(k), values=v[:50], out_values=torch.empty_like(v))
+    with pytest.raises(AssertionError):
+        vx.sort_into(k, torch.empty_like(k), values=v.to(torch.int16), out_values=torch.empty_like(v))
+    with pytest.raises(AssertionError):
+        vx.sort_into(k, torch.empty_like(k), values=v, out_values=torch.empty(100, dtype=torch.int64, device="cuda"))
+    with pytest.raises(AssertionError):
+        vx.sort_into(k, torch.empty(99, dtype=torch.int32, device="cuda"))
+
+
+def test_segments_reject_out_of_range_offsets():
+    import paper_1704_08579_b200 as vx
+
+    x = torch.arange(100, 0, -1, dtype=torch.int32, device="cuda")
+    before = x.clone()
+    for bad in ([0, 50, 120], [0, 60, 40, 100], [-5, 10]):
+        with pytest.raises(AssertionError):
+            vx.sort_segments(x, torch.tensor(bad, dtype=torch.int64, device="cuda"))
+    y = before.clone()
+    vx.sort_segments(y, torch.tensor([0, 100], dtype=torch.int64, device="cuda"))
+    assert torch.equal(y, torch.sort(before).values)
