@@ -121,6 +121,27 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned* smem, 
     return r;
 }
 
+// ------------------------------------------------ shared-memory counters
+// Shared-memory atomics whose result is unused compile to ATOMS.POPC.INC,
+// which merges the lanes of a warp that hit one counter.  RANKING atomics
+// (result used) serialise instead when a warp's lanes share a bucket (sorted,
+// reverse or few-unique inputs); warp_rank_add takes the warp's active lanes
+// and, when they all carry one bucket, lets the first lane reserve for all.
+// Ranks inside a bucket are then a permutation of the per-lane ones (the
+// order of keys inside a bucket is never observable: later passes sort it).
+__device__ __forceinline__ unsigned warp_rank_add(unsigned* cnt, unsigned b) {
+    const unsigned am = __activemask();
+    const int first = __ffs(am) - 1;
+    const unsigned b0 = __shfl_sync(am, b, first);
+    if (__all_sync(am, b == b0)) {
+        const unsigned lane = threadIdx.x & 31;
+        unsigned base = 0;
+        if ((int)lane == first) base = atomicAdd(&cnt[b0], (unsigned)__popc(am));
+        return __shfl_sync(am, base, first) + __popc(am & ((1u << lane) - 1u));
+    }
+    return atomicAdd(&cnt[b], 1u);
+}
+
 // 64-bit hash (splitmix64 finaliser) for deterministic sample positions.
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ULL;

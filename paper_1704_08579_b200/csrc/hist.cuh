@@ -129,6 +129,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 const unsigned b = classify(sb[i * kQsNT + tid]);
+                // result unused: ATOMS.POPC.INC, which already merges the
+                // lanes of a warp that hit one counter (sorted inputs)
                 atomicAdd(&s_hist[b], 1u);
                 ids[bt.base + i * kQsNT + tid] = (unsigned short)b;
             }

@@ -110,6 +110,37 @@ __device__ __forceinline__ void seg_for_each(const K* __restrict__ p, unsigned l
     for (unsigned i = head + nv * VE + threadIdx.x; i < len; i += NT) f(p[i]);
 }
 
+// f(keys, count) for every 16-byte vector of p[0, len) (count = 16 /
+// sizeof(K) consecutive keys; the unaligned head and tail come one key at a
+// time): lets a pass aggregate a vector's keys that share a bucket.
+template <typename K, unsigned NT, typename F>
+__device__ __forceinline__ void seg_for_each_vec(const K* __restrict__ p, unsigned len, F&& f) {
+    constexpr unsigned VE = 16 / sizeof(K);
+    union Vec {
+        uint4 v;
+        K k[VE];
+    };
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const unsigned head = min(len, (unsigned)(((16 - (a & 15)) & 15) / sizeof(K)));
+    for (unsigned i = threadIdx.x; i < head; i += NT) f(&p[i], 1u);
+    const unsigned nv = (len - head) / VE;
+    const uint4* v = reinterpret_cast<const uint4*>(p + head);
+    unsigned j = threadIdx.x;
+    for (; j + 3 * NT < nv; j += 4 * NT) {
+        Vec w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[u].v = v[j + u * NT];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) f(w[u].k, VE);
+    }
+    for (; j < nv; j += NT) {
+        Vec w;
+        w.v = v[j];
+        f(w.k, VE);
+    }
+    for (unsigned i = head + nv * VE + threadIdx.x; i < len; i += NT) f(&p[i], 1u);
+}
+
 template <typename U>
 __device__ __forceinline__ U ql_min(U a, U b) { return a < b ? a : b; }
 template <typename U>
@@ -214,6 +245,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
 #pragma unroll
         for (unsigned q = 0; q < BPT; ++q) sm.cnt[tid * BPT + q] = 0;
         __syncthreads();
+        // (result unused: ATOMS.POPC.INC merges a warp's same-counter lanes)
         seg_for_each<K, NT>(sk, len, [&](K x) { atomicAdd(&sm.cnt[bucket(x)], 1u); });
         __syncthreads();
         unsigned c[BPT], sum = 0;
@@ -259,7 +291,27 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
         // (measured on B200: direct -4 % int32 keys, +26 % kv).
         if constexpr (!KV) {
         __syncthreads();  // cursors complete
-        seg_for_each<K, NT>(sk, len, [&](K x) { ok[atomicAdd(&sm.off[bucket(x)], 1u)] = x; });
+        seg_for_each_vec<K, NT>(sk, len, [&](const K* x, unsigned c) {
+            if (c == 1) {
+                ok[atomicAdd(&sm.off[bucket(x[0])], 1u)] = x[0];
+                return;
+            }
+            constexpr unsigned VE = 16 / sizeof(K);
+            unsigned b[VE];
+#pragma unroll
+            for (unsigned r = 0; r < VE; ++r) b[r] = bucket(x[r]);
+            bool run = true;
+#pragma unroll
+            for (unsigned r = 1; r < VE; ++r) run &= b[r] == b[0];
+            if (run) {  // a sorted run inside one bucket: one reservation
+                const unsigned p0 = atomicAdd(&sm.off[b[0]], VE);
+#pragma unroll
+                for (unsigned r = 0; r < VE; ++r) ok[p0 + r] = x[r];
+                return;
+            }
+#pragma unroll
+            for (unsigned r = 0; r < VE; ++r) ok[atomicAdd(&sm.off[b[r]], 1u)] = x[r];
+        });
         } else {
         for (unsigned t0 = 0; t0 < len; t0 += TILE) {
             const unsigned tn = min(TILE, len - t0);

@@ -851,8 +851,10 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
     // rank inside the tile, packed next to the bucket id: (bucket << 16) | rank
     unsigned br[IPT];
 #pragma unroll
-    for (int i = 0; i < IPT; ++i)
-        br[i] = ((validmask >> i) & 1u) ? ((bk[i] << 16) | atomicAdd(&sm.cnt[bk[i]], 1u)) : 0u;
+    for (int i = 0; i < IPT; ++i) {
+        br[i] = 0u;
+        if ((validmask >> i) & 1u) br[i] = (bk[i] << 16) | atomicAdd(&sm.cnt[bk[i]], 1u);
+    }
     __syncthreads();
     // exclusive scan of counts over nb (<= 2*NT) buckets: 2 per thread
     const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;

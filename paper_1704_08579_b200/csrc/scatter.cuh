@@ -92,10 +92,21 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         // rank by the bucket id the histogram pass stored: (bucket << 16) | rank within the tile
         unsigned br[IPT];
         if (g.tn == TILE) {
+            // a warp whose IPT x 32 keys share one bucket (sorted / reverse /
+            // few-unique inputs) reserves their ranks with one atomic
+            const unsigned b0 = __shfl_sync(0xffffffffu, (unsigned)id[0], 0);
+            bool same = true;
 #pragma unroll
-            for (int i = 0; i < IPT; ++i) {
-                const unsigned b = id[i];
-                br[i] = (b << 16) | atomicAdd(&cnt[b], 1u);
+            for (int i = 0; i < IPT; ++i) same &= id[i] == b0;
+            if (__all_sync(0xffffffffu, same)) {
+                unsigned base = 0;
+                if ((threadIdx.x & 31) == 0) base = atomicAdd(&cnt[b0], 32u * IPT);
+                base = __shfl_sync(0xffffffffu, base, 0) + (threadIdx.x & 31);
+#pragma unroll
+                for (int i = 0; i < IPT; ++i) br[i] = (b0 << 16) | (base + 32u * i);
+            } else {
+#pragma unroll
+                for (int i = 0; i < IPT; ++i) br[i] = ((unsigned)id[i] << 16) | atomicAdd(&cnt[id[i]], 1u);
             }
         } else {
 #pragma unroll

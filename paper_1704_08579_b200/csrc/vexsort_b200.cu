@@ -19,6 +19,7 @@
 #include "scatter.cuh"
 #include "hist.cuh"
 #include "local.cuh"
+#include "localc.cuh"
 
 using namespace vx;
 
@@ -229,6 +230,7 @@ struct SortCtx {
     uint64_t n, seed, ql_target, ql_cap;
     unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags;
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
+    bool cluster_local;  // CTA-local level in distributed shared memory (localc.cuh)
 };
 
 template <typename K, typename V>
@@ -269,11 +271,15 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
     }
     VX_LAUNCHED();
     if (x.ql_cap) {
-        // medium children: CTA-local last level + leaves (data in dst, other buffer = src side)
+        // medium children: CTA-local last level + leaves (data in dst)
         Launch l(KC_LOCAL, st, timed ? 1 : 0, timed);
-        qs_local_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QlSmem<K, V>), st>>>(
-            x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals, x.keys,
-            x.vals, x.leaf);
+        if (x.cluster_local)
+            qs_localc_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QcSmem<K, V>), st>>>(
+                x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, x.keys, x.vals, x.leaf);
+        else  // single-CTA variant: intermediate through L2 in the other buffer
+            qs_local_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QlSmem<K, V>), st>>>(
+                x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
+                x.keys, x.vals, x.leaf);
         ++kernels;
         VX_LAUNCHED();
     }
@@ -543,7 +549,11 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         x.ql_target =
             (uint64_t)std::min((double)QlCfg<K, V>::TARGET, std::max((double)QlCfg<K, V>::TMIN, ceil(t)));
     }
-    x.ql_cap = ql_on ? QlCfg<K, V>::CAP : 0;
+    // the distributed-shared-memory variant (localc.cuh) is opt-in: measured
+    // slower than the single-CTA level on B200
+    static const bool cluster_local = getenv("VX_QL_CLUSTER") != nullptr;
+    x.cluster_local = cluster_local;
+    x.ql_cap = ql_on ? (x.cluster_local ? QcCfg<K, V>::CAP : QlCfg<K, V>::CAP) : 0;
     // n <= the finish capacity: the whole array is one finish item whose
     // source is the input
     x.as_fin = n <= L::LOCAL ? 1u : 0u;
@@ -555,7 +565,35 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     x.g_hist = x.sms * VX_OCC(qs_hist_kernel<K>, kQsNT, hist_smem_bytes<K>());
     x.g_scat = x.sms * VX_OCC((qs_scatter_kernel<K, V>), kQsNT, sizeof(ScatterPipeSmem<K, V>));
     x.g_fin = x.sms * VX_OCC((qs_finish_kernel<K, V>), kFinNT, sizeof(FinSmem<K, V>));
-    x.g_loc = x.sms * VX_OCC((qs_local_kernel<K, V>), kQlNT, sizeof(QlSmem<K, V>));
+    if (x.cluster_local) {
+        // persistent: as many 4-CTA clusters as fit at once
+        static int ncl_cache[kMaxDev] = {};
+        int& ncl = ncl_cache[cur_dev()];
+        if (!ncl) {
+            auto* kern = qs_localc_kernel<K, V>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QcSmem<K, V>));
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(kQcC * 64);
+            lc.blockDim = dim3(kQlNT);
+            lc.dynamicSmemBytes = sizeof(QcSmem<K, V>);
+            cudaLaunchAttribute at;
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = kQcC;
+            at.val.clusterDim.y = 1;
+            at.val.clusterDim.z = 1;
+            lc.attrs = &at;
+            lc.numAttrs = 1;
+            int v = 0;
+            if (cudaOccupancyMaxActiveClusters(&v, (const void*)kern, &lc) != cudaSuccess || v <= 0) {
+                cudaGetLastError();
+                v = x.sms / kQcC;
+            }
+            ncl = v;
+        }
+        x.g_loc = ncl * kQcC;
+    } else {
+        x.g_loc = x.sms * VX_OCC((qs_local_kernel<K, V>), kQlNT, sizeof(QlSmem<K, V>));
+    }
     x.g_seg = 2 * x.sms;
 
     bool eager = false;
