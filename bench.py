@@ -236,7 +236,7 @@ def make_step(spec, vx, L, dev, rank, world, seed):
             out = torch.empty_like(src)
             w["step"] = lambda: vx.sort_into(src, out, check=False)  # noqa: E731
         else:
-            w["step"] = lambda: vx.sharded_sort(src, seed=seed)  # noqa: E731
+            w["step"] = lambda: vx.sharded_sort(src, seed=seed, exchange=spec.get("exchange", "collective"))  # noqa: E731
         w.update(src=src, units=n, unit_bytes=2 * esz)
     elif kind == "sort":
         n = spec["n"]
@@ -642,10 +642,14 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=2, help="steps of the per-kernel profiled pass")
+    ap.add_argument("--exchange", default="collective", choices=["collective", "fused"],
+                    help="sharded sort (N>1): NCCL all-to-all, or the fused partition+NVLink-store exchange")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     spec = workload_spec(args.workload, args.n)
+    if spec["kind"] == "sharded":
+        spec["exchange"] = args.exchange
     dtype = {"i32": "int32", "f64": "float64"}[spec["dtype"]]
     cfg = {"workload": args.workload, **{k: v for k, v in spec.items() if k not in ("kind", "scaling")}}
     base = {"metric": METRIC, "unit": "Gelem/s", "higher_is_better": True, "scaling": spec["scaling"],
@@ -665,7 +669,8 @@ def main():
 
     rank, world, local = dist_setup(args.gpus)
     r = run_ours(args, spec, rank, world, local)
-    cfg["parallelism"] = ((f"sample sort over {world} ranks (NCCL all-to-all)" if world > 1 else
+    xname = "NCCL all-to-all" if spec.get("exchange") != "fused" else "fused partition + IPC/NVLink stores"
+    cfg["parallelism"] = ((f"sample sort over {world} ranks ({xname})" if world > 1 else
                            "single GPU (P=1 sample sort = the local hybrid sort; no exchange)")
                           if spec["kind"] == "sharded"
                           else ("replicas" if world > 1 else "single GPU"))

@@ -133,6 +133,33 @@ int vx_bucket_partition(int dtype, const void *in_keys, void *out_keys, int64_t 
 int vx_select_splitters(int dtype, const void *d_sample_keys, const uint64_t *d_sample_idx, int64_t count,
                         int nparts, void *d_out_keys, uint64_t *d_out_idx, vx_stream_t stream);
 
+/* Fused exchange: the bucket partition writes each
+ * destination's run STRAIGHT into that destination's buffer -- on a
+ * multi-GPU box a peer GPU's receive buffer mapped with CUDA IPC, so the
+ * partition's stores are the NVLink transfer and no all-to-all copy
+ * follows.  vx_bucket_counts: per-destination counts only (histogram pass).
+ * vx_bucket_scatter_to: destination b's keys land in
+ * ((K*)d_dst_ptrs[b])[d_dst_offsets[b] ...] (both device arrays of
+ * nsplit+1 uint64; ws as for vx_bucket_partition).  The caller orders the
+ * kernel before any reader (stream sync + a host barrier across ranks). */
+int vx_bucket_counts(int dtype, const void *in_keys, int64_t n, uint64_t global_offset, const void *d_split_keys,
+                     const uint64_t *d_split_idx, int nsplit, unsigned long long *d_counts, vx_stream_t stream);
+int vx_bucket_scatter_to(int dtype, const void *in_keys, int64_t n, uint64_t global_offset,
+                         const void *d_split_keys, const uint64_t *d_split_idx, int nsplit,
+                         const unsigned long long *d_dst_ptrs, const unsigned long long *d_dst_offsets, void *ws,
+                         size_t ws_bytes, vx_stream_t stream);
+/* Receive buffers shared across processes: a cudaMalloc'd buffer, its
+ * 64-byte IPC handle, and mapping / unmapping a peer's handle (peer access
+ * enabled lazily).  vx_sort_from_ptr: vx_sort_into from a raw device
+ * address (e.g. the receive buffer) into out_keys. */
+int vx_ipc_alloc(size_t bytes, void **dptr);
+int vx_ipc_free(void *dptr);
+int vx_ipc_handle(const void *dptr, void *handle64);
+int vx_ipc_open(const void *handle64, void **dptr);
+int vx_ipc_close(void *dptr);
+int vx_sort_from_ptr(int dtype, uint64_t in_keys, void *out_keys, int64_t n, const vx_sort_config *cfg, void *ws,
+                     size_t ws_bytes, vx_stream_t stream);
+
 /* Seeded synthetic inputs generated on the device (bench only).
  * dist: 0 uniform (int32 full range / f64 [-1e6,1e6)), 1 sorted, 2 reverse,
  * 3 few-unique [0,16), 4 standard normal (f64), 5 uniform [0,2^31) int32,

@@ -75,6 +75,14 @@ def _declare(L):
         "vx_bucket_partition_workspace_bytes": ([i32, i32], sz),
         "vx_bucket_partition": ([i32, vp, vp, i64, u64, vp, vp, i32, vp, vp, sz, vp], i32),
         "vx_select_splitters": ([i32, vp, vp, i64, i32, vp, vp, vp], i32),
+        "vx_bucket_counts": ([i32, vp, i64, u64, vp, vp, i32, vp, vp], i32),
+        "vx_bucket_scatter_to": ([i32, vp, i64, u64, vp, vp, i32, vp, vp, vp, sz, vp], i32),
+        "vx_ipc_alloc": ([sz, ctypes.POINTER(ctypes.c_void_p)], i32),
+        "vx_ipc_free": ([vp], i32),
+        "vx_ipc_handle": ([vp, vp], i32),
+        "vx_ipc_open": ([vp, ctypes.POINTER(ctypes.c_void_p)], i32),
+        "vx_ipc_close": ([vp], i32),
+        "vx_sort_from_ptr": ([i32, u64, vp, i64, ctypes.POINTER(SortConfigC), vp, sz, vp], i32),
         "vx_generate": ([i32, i32, vp, i64, u64, u64, i64, vp], i32),
         "vx_verify": ([i32, vp, vp, i64, i32, vp, i64, vp, vp], i32),
         "vx_host_quicksort": ([i32, vp, i64, i64, i64, i32, i32, i32, u64], i32),

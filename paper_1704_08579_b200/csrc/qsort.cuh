@@ -837,6 +837,7 @@ struct ScatterSmem {
     unsigned long long gbase[kMaxBkt + 1];
     CellTable<typename OKey<K>::U> ct;  // splitters + cell lookup table
     typename KeyRep<K>::I spl[256];     // (key, index) splitters of the sharded bucket partition
+    unsigned long long dstp[256];       // fused exchange: destination base pointer per bucket
     unsigned scan[kQsNT / 32 + 1];
 };
 
@@ -846,7 +847,8 @@ struct ScatterSmem {
 template <typename K, typename V, int IPT>
 __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)[IPT], const V (&v)[IPT],
                                              const unsigned (&bk)[IPT], unsigned validmask, unsigned nb,
-                                             unsigned long long* cursor, K* dst_k, V* dst_v, unsigned tn) {
+                                             unsigned long long* cursor, K* dst_k, V* dst_v, unsigned tn,
+                                             bool per_bucket_dst = false) {
     constexpr bool KV = HasVal<V>::value;
     // rank inside the tile, packed next to the bucket id: (bucket << 16) | rank
     unsigned br[IPT];
@@ -883,7 +885,10 @@ __device__ __forceinline__ void tile_scatter(ScatterSmem<K, V>& sm, const K (&k)
     for (unsigned j = threadIdx.x; j < tn; j += kQsNT) {
         const unsigned b = sm.b[j];
         const unsigned long long pos = sm.gbase[b] + (j - sm.loc[b]);
-        dst_k[pos] = sm.k[j];
+        // fused exchange: bucket b's run goes straight into destination b's
+        // buffer (a peer GPU's receive buffer mapped over NVLink)
+        K* dk = per_bucket_dst ? reinterpret_cast<K*>(sm.dstp[b]) : dst_k;
+        dk[pos] = sm.k[j];
         if constexpr (KV) dst_v[pos] = sm.v[j];
     }
 }
@@ -964,7 +969,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) bp_scatter_kernel(const K
                                                            K* __restrict__ dst_k, V* __restrict__ dst_v, uint64_t n,
                                                            uint64_t gofs, const K* __restrict__ spk,
                                                            const uint64_t* __restrict__ spi, unsigned m,
-                                                           unsigned long long* __restrict__ cursor) {
+                                                           unsigned long long* __restrict__ cursor,
+                                                           const unsigned long long* __restrict__ dst_ptrs) {
     constexpr bool KV = HasVal<V>::value;
     constexpr int IPT = QsTile<K>::IPT, TILE = kQsNT * IPT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -974,6 +980,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) bp_scatter_kernel(const K
         sm.spl[i] = KeyRep<K>::to(spk[i]);
         s_i[i] = spi[i];
     }
+    if (dst_ptrs)
+        for (unsigned i = threadIdx.x; i <= m; i += kQsNT) sm.dstp[i] = dst_ptrs[i];
     const unsigned nb = m + 1;
     const uint64_t ntiles = (n + TILE - 1) / TILE;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -996,7 +1004,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) bp_scatter_kernel(const K
                 valid |= 1u << i;
             }
         }
-        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, cursor, dst_k, dst_v, tn);
+        tile_scatter<K, V, IPT>(sm, k, v, bk, valid, nb, cursor, dst_k, dst_v, tn, dst_ptrs != nullptr);
     }
 }
 

@@ -890,6 +890,54 @@ int64_t host_partition(int dtype, void* keys, void* vals, int64_t lo, int64_t hi
 
 }  // namespace
 
+namespace {
+// mode 0: counts + grouped copy into out (hist, scan, scatter); mode 1:
+// counts only; mode 2: scatter only, cursors from d_offsets, runs into
+// per-destination buffers d_dst_ptrs (the fused exchange)
+template <typename K>
+int bucket_pass(int mode, const K* in, K* out, int64_t n, uint64_t gofs, const K* spk, const uint64_t* spi,
+                int nsplit, unsigned long long* d_counts, const unsigned long long* d_offsets,
+                const unsigned long long* d_dst_ptrs, unsigned long long* cursor, cudaStream_t st) {
+    const int sms = num_sms();
+    if (mode != 2) {
+        VX_CUDA(cudaMemsetAsync(d_counts, 0, (nsplit + 1) * 8, st));
+        if (n == 0) return VX_OK;
+        bp_hist_kernel<K><<<sms * 8, kQsNT, 0, st>>>(in, n, gofs, spk, spi, nsplit, d_counts);
+        VX_LAUNCHED();
+        if (mode == 1) return VX_OK;
+        bp_scan_kernel<<<1, 256, 0, st>>>(d_counts, nsplit + 1, cursor);
+        VX_LAUNCHED();
+    } else {
+        if (n == 0) return VX_OK;
+        VX_CUDA(cudaMemcpyAsync(cursor, d_offsets, (nsplit + 1) * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    const int occ = VX_OCC((bp_scatter_kernel<K, NoVal>), kQsNT, sizeof(ScatterSmem<K, NoVal>));
+    bp_scatter_kernel<K, NoVal><<<sms * occ, kQsNT, sizeof(ScatterSmem<K, NoVal>), st>>>(
+        in, nullptr, out, nullptr, n, gofs, spk, spi, nsplit, cursor, mode == 2 ? d_dst_ptrs : nullptr);
+    VX_LAUNCHED();
+    return VX_OK;
+}
+
+int bucket_dispatch(int mode, int dtype, const void* in, void* out, int64_t n, uint64_t gofs, const void* spk,
+                    const uint64_t* spi, int nsplit, unsigned long long* d_counts,
+                    const unsigned long long* d_offsets, const unsigned long long* d_dst_ptrs, void* ws,
+                    size_t ws_bytes, cudaStream_t st) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (nsplit < 0 || nsplit > kMaxSplit || n < 0) return fail(VX_EINVAL, "bad argument");
+    if ((mode != 2 && !d_counts) || (mode == 2 && (!d_offsets || !d_dst_ptrs))) return fail(VX_EINVAL, "bad argument");
+    if (mode != 1 && (!ws || ws_bytes < vx_bucket_partition_workspace_bytes(dtype, nsplit)))
+        return fail(VX_EWORKSPACE, "workspace");
+    auto* cursor = static_cast<unsigned long long*>(ws);
+    Launch lch(KC_BUCKET, st, mode == 0 ? 3 : 1);
+    if (g_prof.on) prof_elems(KC_BUCKET, n);
+    if (dtype == VX_I32)
+        return bucket_pass<int32_t>(mode, (const int32_t*)in, (int32_t*)out, n, gofs, (const int32_t*)spk, spi,
+                                    nsplit, d_counts, d_offsets, d_dst_ptrs, cursor, st);
+    return bucket_pass<double>(mode, (const double*)in, (double*)out, n, gofs, (const double*)spk, spi, nsplit,
+                               d_counts, d_offsets, d_dst_ptrs, cursor, st);
+}
+}  // namespace
+
 // ====================================================================== C ABI
 extern "C" {
 
@@ -1036,40 +1084,65 @@ size_t vx_bucket_partition_workspace_bytes(int dtype, int nsplit) {
     return align_up((size_t)(nsplit + 1) * 8);
 }
 
+
 int vx_bucket_partition(int dtype, const void* in_keys, void* out_keys, int64_t n, uint64_t global_offset,
                         const void* d_split_keys, const uint64_t* d_split_idx, int nsplit,
                         unsigned long long* d_counts, void* ws, size_t ws_bytes, vx_stream_t stream) {
-    if (int rc = check_dtype(dtype)) return rc;
-    if (nsplit < 0 || nsplit > kMaxSplit || n < 0 || !d_counts) return fail(VX_EINVAL, "bad argument");
-    if (!ws || ws_bytes < vx_bucket_partition_workspace_bytes(dtype, nsplit)) return fail(VX_EWORKSPACE, "workspace");
-    cudaStream_t st = (cudaStream_t)stream;
-    auto* cursor = static_cast<unsigned long long*>(ws);
-    VX_CUDA(cudaMemsetAsync(d_counts, 0, (nsplit + 1) * 8, st));
-    if (n == 0) return VX_OK;
-    const int sms = num_sms();
-    Launch lch(KC_BUCKET, st, 3);
-    if (g_prof.on) prof_elems(KC_BUCKET, n);
-    if (dtype == VX_I32) {
-        using K = int32_t;
-        const int occ = VX_OCC((bp_scatter_kernel<K, NoVal>), kQsNT, sizeof(ScatterSmem<K, NoVal>));
-        bp_hist_kernel<K><<<sms * 8, kQsNT, 0, st>>>((const K*)in_keys, n, global_offset, (const K*)d_split_keys,
-                                                    d_split_idx, nsplit, d_counts);
-        bp_scan_kernel<<<1, 256, 0, st>>>(d_counts, nsplit + 1, cursor);
-        bp_scatter_kernel<K, NoVal><<<sms * occ, kQsNT, sizeof(ScatterSmem<K, NoVal>), st>>>(
-            (const K*)in_keys, nullptr, (K*)out_keys, nullptr, n, global_offset, (const K*)d_split_keys, d_split_idx,
-            nsplit, cursor);
-    } else {
-        using K = double;
-        const int occ = VX_OCC((bp_scatter_kernel<K, NoVal>), kQsNT, sizeof(ScatterSmem<K, NoVal>));
-        bp_hist_kernel<K><<<sms * 8, kQsNT, 0, st>>>((const K*)in_keys, n, global_offset, (const K*)d_split_keys,
-                                                    d_split_idx, nsplit, d_counts);
-        bp_scan_kernel<<<1, 256, 0, st>>>(d_counts, nsplit + 1, cursor);
-        bp_scatter_kernel<K, NoVal><<<sms * occ, kQsNT, sizeof(ScatterSmem<K, NoVal>), st>>>(
-            (const K*)in_keys, nullptr, (K*)out_keys, nullptr, n, global_offset, (const K*)d_split_keys, d_split_idx,
-            nsplit, cursor);
-    }
-    VX_LAUNCHED();
+    return bucket_dispatch(0, dtype, in_keys, out_keys, n, global_offset, d_split_keys, d_split_idx, nsplit,
+                           d_counts, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vx_bucket_counts(int dtype, const void* in_keys, int64_t n, uint64_t global_offset, const void* d_split_keys,
+                     const uint64_t* d_split_idx, int nsplit, unsigned long long* d_counts, vx_stream_t stream) {
+    return bucket_dispatch(1, dtype, in_keys, nullptr, n, global_offset, d_split_keys, d_split_idx, nsplit,
+                           d_counts, nullptr, nullptr, nullptr, 0, (cudaStream_t)stream);
+}
+
+int vx_bucket_scatter_to(int dtype, const void* in_keys, int64_t n, uint64_t global_offset, const void* d_split_keys,
+                         const uint64_t* d_split_idx, int nsplit, const unsigned long long* d_dst_ptrs,
+                         const unsigned long long* d_dst_offsets, void* ws, size_t ws_bytes, vx_stream_t stream) {
+    return bucket_dispatch(2, dtype, in_keys, nullptr, n, global_offset, d_split_keys, d_split_idx, nsplit, nullptr,
+                           d_dst_offsets, d_dst_ptrs, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int vx_ipc_alloc(size_t bytes, void** dptr) {
+    if (!dptr) return fail(VX_EINVAL, "bad argument");
+    *dptr = nullptr;
+    VX_CUDA(cudaMalloc(dptr, bytes ? bytes : 256));
     return VX_OK;
+}
+
+int vx_ipc_free(void* dptr) {
+    if (dptr) VX_CUDA(cudaFree(dptr));
+    return VX_OK;
+}
+
+int vx_ipc_handle(const void* dptr, void* handle) {
+    if (!dptr || !handle) return fail(VX_EINVAL, "bad argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    VX_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    std::memcpy(handle, &h, sizeof h);
+    return VX_OK;
+}
+
+int vx_ipc_open(const void* handle, void** dptr) {
+    if (!handle || !dptr) return fail(VX_EINVAL, "bad argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    VX_CUDA(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return VX_OK;
+}
+
+int vx_ipc_close(void* dptr) {
+    if (dptr) VX_CUDA(cudaIpcCloseMemHandle(dptr));
+    return VX_OK;
+}
+
+int vx_sort_from_ptr(int dtype, uint64_t in_keys, void* out_keys, int64_t n, const vx_sort_config* cfg, void* ws,
+                     size_t ws_bytes, vx_stream_t stream) {
+    return vx_sort_into(dtype, reinterpret_cast<const void*>(in_keys), nullptr, out_keys, nullptr, n, cfg, ws, ws_bytes,
+                        stream);
 }
 
 int vx_select_splitters(int dtype, const void* d_sample_keys, const uint64_t* d_sample_idx, int64_t count,

@@ -119,3 +119,15 @@ def test_sample_positions_are_in_range_and_stratified():
         assert len(p) == min(n, s)
         assert p.min() >= 0 and p.max() < n
         assert np.all(np.diff(p) > 0)  # one per stratum, increasing
+
+
+def test_fused_offsets_pack_sources_in_rank_order():
+    from paper_1704_08579_b200.sharded import fused_offsets
+
+    cm = [[3, 1, 4], [1, 5, 9], [2, 6, 5]]  # cm[q][d]: q sends to d
+    assert fused_offsets(cm, 0) == [0, 0, 0]
+    assert fused_offsets(cm, 1) == [3, 1, 4]
+    assert fused_offsets(cm, 2) == [4, 6, 13]
+    # the last source's run ends exactly at the receive size
+    for d in range(3):
+        assert fused_offsets(cm, 2)[d] + cm[2][d] == sum(cm[q][d] for q in range(3))

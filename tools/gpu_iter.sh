@@ -4,7 +4,7 @@ mkdir -p gpurun_out/it
 timeout 1200 python -m pytest tests -m gpu -x -q -k "${TESTK:-not c5_full_size}" > gpurun_out/it/pytest.log 2>&1
 echo "pytest rc=$? $(tail -1 gpurun_out/it/pytest.log)"
 grep -E "^E |FAILED|Error" gpurun_out/it/pytest.log | head -20
-for w in ${WL:-c5_i32_uniform sort_i32}; do
+for w in ${WL-c5_i32_uniform sort_i32}; do
   for v in ${VARIANTS:-default}; do
     env=""; [ "$v" != default ] && env="$v=1"
     env $env timeout 600 python bench.py --workload $w --steps ${STEPS:-5} --warmup 3 --no-cpu --no-e2e > gpurun_out/it/$w.$v.json 2> gpurun_out/it/$w.$v.err
