@@ -52,9 +52,12 @@ enum {
 /* SortConfig (quicksort.py:28-46).  sort_bound <= 0 selects the default
  * 16*lanes (256 int32 / 128 float64); it is the largest range handed to the
  * bitonic network and must be <= 16*lanes (quicksort.py:49-52).
- * pivot_strategy (0 median3, 1 middle, 2 random) and the two partition flags
- * are accepted for drop-in fidelity; the B200 driver samples its pivots
- * (seeded by pivot_seed) and the flags do not apply to a GPU partition. */
+ * pivot_strategy (0 median3, 1 middle, 2 random; VX_EINVAL otherwise)
+ * selects how the sampled-pivot levels draw their sample: stratified hashed
+ * positions (default), stratum midpoints, or the reference's MMIX LCG seeded
+ * by pivot_seed (see qsort.cuh sample_pos).  The output is the same for all
+ * three.  The two partition flags are CPU store-pattern variants of the
+ * reference partition and do not apply on the GPU (accepted, ignored). */
 typedef struct {
     int64_t sort_bound;
     int32_t pivot_strategy;

@@ -535,13 +535,40 @@ __global__ void qs_loopctl_kernel(const Ctl* tot, cudaGraphConditionalHandle con
 }
 
 // ------------------------------------------------------------ plan
+// Position (in [0, len)) of sample i of S for the sampled-pivot levels, by
+// the reference's pivot_strategy (quicksort.py:55-74, _kernels.py:358-376).
+// A level takes many pivots at once, so each strategy picks the level's
+// SAMPLE the way the reference picks its one pivot index:
+//   0 median3 (default): one sample per stratum [i*len/S, (i+1)*len/S) at a
+//     hashed offset -- stratified, the low-variance robust default;
+//   1 middle: the middle index of every stratum, (lo + hi) // 2 -- no
+//     randomness, like the reference's middle pivot;
+//   2 random: the reference's 64-bit MMIX LCG (quicksort.py:22-25) seeded
+//     with pivot_seed, one draw per sample over the whole segment.
+// The pivots only steer the work; the sorted output is unique.
+constexpr uint64_t kLcgMul = 6364136223846793005ULL, kLcgAdd = 1442695040888963407ULL;
+__device__ __forceinline__ uint64_t sample_pos(unsigned strategy, uint64_t seed, uint64_t start, uint64_t len,
+                                               unsigned i, unsigned S) {
+    if (strategy == 2) {
+        const uint64_t lcg = (seed + start + i) * kLcgMul + kLcgAdd;
+        return __umul64hi(lcg * kLcgMul + kLcgAdd, len);  // lo + lcg mod span, by a high multiply
+    }
+    const uint64_t lo = (uint64_t)i * len / S, hi = (uint64_t)(i + 1) * len / S;  // stratum [lo, hi)
+    const uint64_t span = hi > lo ? hi - lo : 1;
+    if (strategy == 1) return lo + (span - 1) / 2;
+    const uint64_t h = mix64(seed ^ mix64(start * 0x9E3779B97F4A7C15ULL + i));
+    const uint64_t p = lo + __umul64hi(h, span);
+    return p < len ? p : len - 1;
+}
+
 template <typename K, typename V>
 __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ src, Seg* __restrict__ segs,
                                                           Ctl* __restrict__ ctl, K* __restrict__ spl_pool,
                                                           unsigned long long* __restrict__ bkt_pool,
                                                           unsigned* __restrict__ tile_owner, unsigned cap_spl,
                                                           unsigned cap_bkt, unsigned cap_tiles, uint64_t sort_seed,
-                                                          const Ctl* __restrict__ tot, uint64_t ql_target) {
+                                                          const Ctl* __restrict__ tot, uint64_t ql_target,
+                                                          unsigned strategy) {
     constexpr int TILE = qs_tile<K>();
     __shared__ K s_samp[kMaxSample];
     __shared__ unsigned s_scan[kPlanNT / 32 + 1];
@@ -621,8 +648,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
 #pragma unroll 4
         for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
-            const uint64_t h = mix64(seed ^ mix64(start * 0x9E3779B97F4A7C15ULL + i));
-            s_samp[i] = src[start + __umul64hi(h, len)];  // uniform in [0, len) without a 64-bit division
+            s_samp[i] = src[start + sample_pos(strategy, seed, start, len, i, S)];
         }
         __syncthreads();
 #ifdef VX_PLAN_CTA_BITONIC

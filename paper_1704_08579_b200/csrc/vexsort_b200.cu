@@ -228,7 +228,7 @@ struct SortCtx {
     const K* root_scr_k;
     const V* root_scr_v;
     uint64_t n, seed, ql_target, ql_cap;
-    unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags;
+    unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags, strategy;
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
     bool cluster_local;  // CTA-local level in distributed shared memory (localc.cuh)
 };
@@ -249,7 +249,8 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
     {
         Launch l(KC_PLAN, st, timed ? 1 : 0, timed);
         qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, x.segs[p], c, x.spl, x.bkt, x.towner, x.cap_spl,
-                                                         x.cap_bkt, x.cap_tiles, x.seed, tot, x.ql_target);
+                                                         x.cap_bkt, x.cap_tiles, x.seed, tot, x.ql_target,
+                                                         x.strategy);
     }
     VX_LAUNCHED();
     {
@@ -420,7 +421,7 @@ int launch_sort_graph(const SortCtx<K, V>& x, cudaStream_t st) {
     key.p[4] = x.ctl;
     key.n = x.n;
     key.seed = x.seed;
-    key.leaf = x.leaf;
+    key.leaf = x.leaf | ((uint64_t)x.strategy << 32);
     std::lock_guard<std::mutex> lk(g_graphs.mu);
     cudaGraphExec_t exec = nullptr;
     for (auto& e : g_graphs.v)
@@ -521,6 +522,8 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     x.qls = reinterpret_cast<QlItemT*>(w + lay.off_ql);
     x.n = n;
     x.seed = mix64(cfg ? cfg->pivot_seed : 0);
+    x.strategy = cfg ? (unsigned)cfg->pivot_strategy : 0u;
+    if (x.strategy > 2) return fail(VX_EINVAL, "unknown pivot strategy");
     x.cap_seg = (unsigned)lay.cap_seg;
     x.cap_spl = (unsigned)lay.cap_spl;
     x.cap_bkt = (unsigned)lay.cap_bkt;

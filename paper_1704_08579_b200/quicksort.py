@@ -29,10 +29,14 @@ class SortConfig:
 
     sort_bound: largest range handed to the bitonic network (default
     16*lanes: 256 int32 / 128 float64; must not exceed it).  pivot_strategy
-    is validated like the reference's; the B200 driver always samples its
-    pivots (seeded by pivot_seed), so the strategy cannot change the (unique)
-    sorted output.  skip_empty_stores / swap_buffered are CPU store-pattern
-    options of the reference partition and are accepted as no-ops.
+    is validated like the reference's and selects how the device levels draw
+    the sample their pivots come from (a level takes up to 255 pivots at
+    once): "median3" stratified hashed positions, "middle" stratum
+    midpoints, "random" the reference's MMIX LCG seeded by pivot_seed
+    (csrc/qsort.cuh sample_pos).  The sorted output is unique, so the
+    strategy cannot change it.  skip_empty_stores / swap_buffered are CPU
+    store-pattern options of the reference partition and are accepted as
+    no-ops.
     """
 
     sort_bound: int | None = None

@@ -51,6 +51,12 @@ def import_reference():
     if not os.path.isdir(dst):
         os.makedirs(REF_COPY, exist_ok=True)
         shutil.copytree(REF_SRC, dst)
+    # the reference's own tests, run through integration/_kernels_b200.py by
+    # tests/test_gpu_integration.py (baseline/_ref is git-ignored; it travels
+    # to the GPU box with the working tree)
+    tdst = os.path.join(REF_COPY, "tests")
+    if not os.path.isdir(tdst):
+        shutil.copytree(os.path.join(os.path.dirname(os.path.dirname(REF_SRC)), "tests"), tdst)
     sys.path.insert(0, REF_COPY)
     import vexsort  # noqa: F401
 

@@ -199,3 +199,33 @@ def test_segments_reject_out_of_range_offsets():
     y = before.clone()
     vx.sort_segments(y, torch.tensor([0, 100], dtype=torch.int64, device="cuda"))
     assert torch.equal(y, torch.sort(before).values)
+
+
+@pytest.mark.parametrize("tdt,n", [(torch.int32, 1 << 20), (torch.int32, 1 << 24), (torch.float64, 1 << 23),
+                                   (torch.int32, 30000)])
+def test_pivot_strategies_same_output(tdt, n):
+    """pivot_strategy steers the sampled levels (stratified / middle / LCG);
+    every strategy and seed yields the one sorted output."""
+    import paper_1704_08579_b200 as vx
+    from paper_1704_08579_b200.verify import digest, generate
+
+    for dist in ("uniform", "sorted", "few"):
+        src = generate(tdt, dist, n, seed=21)
+        want = None
+        for strategy in ("median3", "middle", "random"):
+            for seed in (0, 12345):
+                out = torch.empty_like(src)
+                vx.sort_into(src, out, vx.SortConfig(pivot_strategy=strategy, pivot_seed=seed))
+                d = digest(out)
+                assert d.inversions == 0
+                if want is None:
+                    want = (d.positional, digest(src, order=False).multiset())
+                assert (d.positional, d.multiset()) == want, (strategy, seed, dist)
+    # skewed keys take the sampled-pivot fallback of the local level
+    x = (torch.randn(n, device="cuda", dtype=torch.float64).exp() * 1000).to(tdt)
+    outs = []
+    for strategy in ("median3", "middle", "random"):
+        out = torch.empty_like(x)
+        vx.sort_into(x, out, vx.SortConfig(pivot_strategy=strategy, pivot_seed=7))
+        outs.append(out)
+    assert torch.equal(outs[0], torch.sort(x).values) and torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])

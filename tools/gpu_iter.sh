@@ -1,7 +1,7 @@
 # iteration loop on the GPU box: GPU tests (filter in $TESTK), then bench lines
 #   TESTK="expr" WL="w1 w2" AB=1 bash tools/gpu_iter.sh
 mkdir -p gpurun_out/it
-timeout 1200 python -m pytest tests -m gpu -x -q -k "${TESTK:-not c5_full_size}" > gpurun_out/it/pytest.log 2>&1
+timeout ${PYT_TIMEOUT:-1200} python -m pytest tests -m gpu -x -q --timeout ${TEST_TIMEOUT:-600} -k "${TESTK:-not c5_full_size}" > gpurun_out/it/pytest.log 2>&1
 echo "pytest rc=$? $(tail -1 gpurun_out/it/pytest.log)"
 grep -E "^E |FAILED|Error" gpurun_out/it/pytest.log | head -20
 for w in ${WL-c5_i32_uniform sort_i32}; do
