@@ -22,6 +22,8 @@
 // key/value comparators use a strict-inversion predicate and selects.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace vx {
@@ -41,10 +43,18 @@ __device__ __forceinline__ uint64_t kmax(uint64_t a, uint64_t b) { return a < b 
 // its group of G lanes).  Fewer lanes and more registers per lane turn
 // cross-lane rounds (shuffle + two selects per slot) into in-register
 // rounds (one min/max per slot).
-template <typename K, typename V, int E, int G = 32>
+//
+// MIX (int32 keys only): integer min / max issue on the half-rate ALU pipe,
+// which bounds a keys-only network.  Two of every three in-register
+// comparators compute the maximum as a + b - min(a, b) with two IMADs (the
+// FMA pipe, idle otherwise; exact in two's complement), which balances the
+// two pipes.  The multiplier is the launch's gridDim.y (= 1), opaque to
+// ptxas, so the multiply-adds are not folded back into ALU adds.
+template <typename K, typename V, int E, int G = 32, bool MIX = false>
 struct WarpBitonic {
     static constexpr int P = G * E;
     static constexpr bool KV = HasVal<V>::value;
+    static constexpr bool MIXED = MIX && !KV && std::is_same<K, int32_t>::value;
 
     // one comparator round with XOR distance MASK over all P slots
     template <int MASK>
@@ -62,6 +72,19 @@ struct WarpBitonic {
                         const V x = v[r], y = v[r2];
                         v[r] = sw ? y : x;
                         v[r2] = sw ? x : y;
+                    } else if constexpr (MIXED) {
+                        if ((r + (r >> 2)) % 3 != 0) {
+                            const int one = (int)gridDim.y;
+                            const int mn = min((int)a, (int)b);
+                            int t, mx;
+                            asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(t) : "r"((int)a), "r"(one), "r"((int)b));
+                            asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(mx) : "r"(mn), "r"(-one), "r"(t));
+                            k[r] = (K)mn;
+                            k[r2] = (K)mx;
+                        } else {
+                            k[r] = kmin(a, b);
+                            k[r2] = kmax(a, b);
+                        }
                     } else {
                         k[r] = kmin(a, b);
                         k[r2] = kmax(a, b);

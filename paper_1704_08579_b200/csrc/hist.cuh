@@ -90,10 +90,13 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     bool radix = false;
     U rlo = 0;
     CellParams<U> cp{};
-    // radix-mode segments: bucket = (code - lo) >> shift (clamped: keys lie
-    // in [lo, hi] by construction)
+    // equal-width segments: bucket = umulhi(code - lo, mul) (keys lie in
+    // [lo, hi] by construction, so the bucket is < nb)
     auto classify = [&](K key) -> unsigned {
-        if (radix) return (unsigned)min((U)(nb - 1), (U)((OKey<K>::of(key) - rlo) >> rsh));
+        if (radix) {
+            const uint32_t d = (uint32_t)(OKey<K>::of(key) - rlo);
+            return min(nb - 1, rsh ? __umulhi(d, rsh) : d);
+        }
         return ct_classify(s_ct, cp, key);
     };
     unsigned stage = 0, par = 0;          // this tile's stage and phase parity
@@ -118,7 +121,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             nb = sg.nb;
             radix = sg.mode == 1;
             rlo = (U)sg.lo;
-            rsh = sg.shift;
+            rsh = sg.mul;
             if (!radix) cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
             for (unsigned b = tid; b < nb; b += kQsNT) s_hist[b] = 0;
             __syncthreads();

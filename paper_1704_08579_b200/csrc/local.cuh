@@ -59,6 +59,24 @@ struct QlCfg {
 
 using QlItem = QlItemT;
 
+// Phase clocks of the CTA-local level (tuning builds only, -DVX_QL_PHASES):
+// SM cycles summed over CTAs for range / count / scan / scatter / networks.
+#ifdef VX_QL_PHASES
+__device__ unsigned long long g_ql_phase[8];
+#define VX_QL_TICK(i)                                                   \
+    do {                                                                \
+        if (threadIdx.x == 0) {                                         \
+            const long long t_ = clock64();                             \
+            atomicAdd(&g_ql_phase[i], (unsigned long long)(t_ - tick)); \
+            tick = t_;                                                  \
+        }                                                               \
+    } while (0)
+#else
+#define VX_QL_TICK(i) \
+    do {              \
+    } while (0)
+#endif
+
 template <typename K, typename V>
 struct QlSmem {
     using C = QlCfg<K, V>;
@@ -170,6 +188,9 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
     const unsigned nitems = ctl->ql_ctr;
     const unsigned wmax = min(leaf, 256u);
     unsigned long long done = 0;
+#ifdef VX_QL_PHASES
+    long long tick = clock64();
+#endif
     for (unsigned it = blockIdx.x; it < nitems; it += gridDim.x) {
         const uint64_t start = items[it].start;
         const unsigned len = (unsigned)items[it].len;
@@ -224,6 +245,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
             __syncthreads();
             continue;
         }
+        VX_QL_TICK(0);
         // ---- 2. interpolation buckets: b = floor(d * nb / (range + 1))
         unsigned nb = min(C::NB, max(1u, (len + C::LT - 1) / C::LT));
         const U range = hi - lo;
@@ -248,6 +270,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
         // (result unused: ATOMS.POPC.INC merges a warp's same-counter lanes)
         seg_for_each<K, NT>(sk, len, [&](K x) { atomicAdd(&sm.cnt[bucket(x)], 1u); });
         __syncthreads();
+        VX_QL_TICK(1);
         unsigned c[BPT], sum = 0;
         bool over = false;
 #pragma unroll
@@ -280,6 +303,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
                 ex += c[q];
             }
         }
+        VX_QL_TICK(2);
         // ---- 3. scatter into the other buffer, bucket-major
         K* ok = oth_k + start;
         V* ov = KV ? oth_v + start : nullptr;
@@ -370,6 +394,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
         // ---- 4. every bucket through the bitonic network into the output
         if (tid == 0) sm.next = 0;
         __syncthreads();  // bucket runs written (CTA-scope visibility of global stores)
+        VX_QL_TICK(3);
 #ifndef VX_QL_DYNAMIC
         // buckets are near-equal (interpolation over a narrow range), so warps
         // take them round-robin: no shared counter between networks
@@ -393,6 +418,7 @@ __global__ void __launch_bounds__(kQlNT, QlMinBlocks<V>::value) qs_local_kernel(
 #endif
         done += len;
         __syncthreads();
+        VX_QL_TICK(4);
     }
     if (tid == 0 && done) atomicAdd(&ctl->loc_elems, done);
 }

@@ -73,14 +73,15 @@ struct FinCap {
 
 // A level segment.  mode 0: partitioned around m sampled pivots into
 // nb = 2m+1 buckets (ranges and equal-to-pivot buckets).  mode 1 (a segment
-// whose key-code bounds [lo, hi] are known from its parent): nb buckets of
-// 2^shift consecutive codes each, bucket = (code - lo) >> shift -- evenly
-// spaced pivots, classified with a subtract and a shift.
+// whose key-code bounds [lo, hi] are known from its parent, 4-byte keys): nb
+// equal-width buckets over [lo, hi], bucket = umulhi(code - lo, mul) with
+// mul = floor(nb * 2^32 / (hi - lo + 1)) -- evenly spaced pivots, classified
+// with a subtract and a high multiply (mul = 0: one code per bucket).
 struct Seg {
     unsigned long long start, len;
     unsigned spl_off, m, bkt_off, tile_base;
     unsigned long long lo, hi;  // key-code bounds (lo > hi: unknown)
-    unsigned nb, shift, mode, pad_;
+    unsigned nb, shift, mode, mul;
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -577,45 +578,46 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
     const uint64_t seed = level_seed(sort_seed, tot);
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const uint64_t start = segs[s].start, len = segs[s].len;
-        unsigned mt;
+        using U = typename OKey<K>::U;
+        const uint64_t slo = segs[s].lo, shi = segs[s].hi;
+        // 4-byte keys only: float64 codes change density at every binade,
+        // which unbalances equal-width buckets (measured slower)
+#ifndef VX_NO_RADIX
+        const bool radix = sizeof(K) == 4 && slo < shi;
+#else
+        const bool radix = false;
+#endif
+        unsigned mt, rb = 0;
         if (ql_target == 0 || len <= 3 * ql_target) {
             // aim the buckets at half the finish capacity
             const uint64_t mt64 = len / (FinCap<K, V>::value / 2);
             mt = (unsigned)max((uint64_t)2, min((uint64_t)kMaxSplit, mt64));
+            rb = mt + 1;
         } else {
             // aim the leaves of the remaining levels at the CTA-local level's
             // target, fan-out balanced over them: L levels of r^(1/L) buckets,
-            // r = len / target.  L counts against TWICE the target
-            // (kQlSlack): the CTA-local level takes up to 3x the target, so
-            // leaves up to 2x (x1.25 sampling spread) still fit.  Counting
-            // against the target itself sent every level-0 bucket even
-            // slightly above 256 x target (half of them at n = 2^32) through
-            // two more levels of fan-out ~17 instead of one of 256.
+            // r = len / target.  A sampled level has up to 256 range buckets
+            // (plus the equal-to-pivot ones), an equal-width level up to 511.
+            // L counts against TWICE the target (kQlSlack): the CTA-local
+            // level takes up to 3x the target, so leaves up to 2x (x1.25
+            // sampling spread) still fit.  Counting against the target itself
+            // sent every level-0 bucket even slightly above fan-out x target
+            // (half of them at n = 2^32) through two more levels.
             const double r = (double)len / (double)ql_target;
-            const double L = ceil(log(r / kQlSlack) / log(256.0) - 1e-9);
+            const double F = radix ? (double)kMaxBkt : (double)(kMaxSplit + 1);
+            const double L = ceil(log(r / kQlSlack) / log(F) - 1e-9);
             const double f = ceil(pow(r, 1.0 / (L < 1.0 ? 1.0 : L)) - 1e-9);
             mt = (unsigned)max(2.0, min((double)kMaxSplit, f - 1.0));
+            rb = (unsigned)max(2.0, min((double)kMaxBkt, f));
         }
-        using U = typename OKey<K>::U;
-        const uint64_t slo = segs[s].lo, shi = segs[s].hi;
-        (void)slo;
-        (void)shi;
-#ifndef VX_RADIX_SPAN
-#define VX_RADIX_SPAN 1
-#endif
-#ifndef VX_NO_RADIX
-        // 4-byte keys only: float64 codes change density at every binade,
-        // which unbalances equal-width buckets (measured slower)
-        if (sizeof(K) == 4 && slo < shi) {
-            // bounds known from the parent: 2^shift-code buckets over
-            // [lo, hi], at most 2(mt+1) of them (at least half non-empty
-            // for locally uniform keys) -- no sample, no pivot table
+        if (radix) {
+            // bounds known from the parent: rb equal-width buckets over
+            // [lo, hi] -- no sample, no pivot table
             const uint64_t range = (uint64_t)(U)(shi - slo);
-            const uint64_t want = (uint64_t)VX_RADIX_SPAN * (mt + 1);
-            const uint64_t bmax = want < (uint64_t)kMaxBkt ? want : (uint64_t)kMaxBkt;
-            unsigned sh = 0;
-            while ((range >> sh) + 1 > bmax) ++sh;
-            const unsigned nb = (unsigned)((range >> sh) + 1);
+            unsigned nb = rb;
+            unsigned mul = 0;
+            if (range + 1 <= (uint64_t)nb) nb = (unsigned)(range + 1);  // one code per bucket
+            else mul = (unsigned)(((uint64_t)nb << 32) / (range + 1));
             if (threadIdx.x == 0) {
                 const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
                 unsigned bo = atomicAdd(&ctl->bkt_ctr, nb);
@@ -633,7 +635,8 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 segs[s].bkt_off = bo;
                 segs[s].tile_base = to;
                 segs[s].nb = nb;
-                segs[s].shift = sh;
+                segs[s].shift = 0;
+                segs[s].mul = mul;
                 segs[s].mode = 1;
             }
             __syncthreads();
@@ -643,7 +646,6 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             __syncthreads();
             continue;
         }
-#endif
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
 #pragma unroll 4
@@ -786,9 +788,13 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
             // and is partitioned around sampled pivots.
             unsigned long long clo = 1, chi = 0;
             if (radix) {
-                const unsigned long long w = 1ull << sg.shift;
-                clo = sg.lo + (unsigned long long)b * w;
-                chi = b + 1 < nb ? sg.lo + (unsigned long long)(b + 1) * w - 1 : sg.hi;
+                // bucket b holds the offsets d with umulhi(d, mul) == b:
+                // [ceil(b * 2^32 / mul), ceil((b + 1) * 2^32 / mul) - 1]
+                auto dlo = [&](unsigned long long bb) -> unsigned long long {
+                    return sg.mul ? ((bb << 32) + sg.mul - 1) / sg.mul : bb;
+                };
+                clo = sg.lo + dlo(b);
+                chi = b + 1 < nb ? sg.lo + dlo(b + 1ull) - 1 : sg.hi;
                 if (2 * c > sg.len) {
                     clo = 1;
                     chi = 0;
@@ -799,7 +805,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                 chi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
             }
             if (c > 0) {
-                const bool final_ = c == 1 || (radix ? (sg.shift == 0) : (b & 1u) != 0);
+                const bool final_ = c == 1 || (radix ? (sg.mul == 0) : (b & 1u) != 0);
                 if (final_) {
                     if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
                         const unsigned nch = (unsigned)((c + kCopyChunk - 1) / kCopyChunk);

@@ -19,6 +19,7 @@
 #include "scatter.cuh"
 #include "hist.cuh"
 #include "local.cuh"
+#include "local2.cuh"
 #include "localc.cuh"
 
 using namespace vx;
@@ -231,6 +232,7 @@ struct SortCtx {
     unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags, strategy;
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
     bool cluster_local;  // CTA-local level in distributed shared memory (localc.cuh)
+    bool global_local;   // CTA-local level with the intermediate in global memory (local.cuh)
 };
 
 template <typename K, typename V>
@@ -277,7 +279,11 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
         if (x.cluster_local)
             qs_localc_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QcSmem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, x.keys, x.vals, x.leaf);
-        else  // single-CTA variant: intermediate through L2 in the other buffer
+        else if (!x.global_local)  // default: intermediate staged in shared memory (local2.cuh)
+            qs_local2_kernel<K, V><<<x.g_loc, kQlNT, sizeof(Q2Smem<K, V>), st>>>(
+                x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
+                x.keys, x.vals, x.leaf);
+        else  // opt-in: intermediate through L2 in the other buffer
             qs_local_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QlSmem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
                 x.keys, x.vals, x.leaf);
@@ -532,11 +538,21 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     // the bitonic leaf bound: the reference's sort_bound when given, else
     // the widest warp network (kWarpSortMax = 256); see DESIGN.md
     x.leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
+    // opt-in variants of the CTA-local level: VX_QL_CLUSTER =
+    // distributed shared memory (localc.cuh), VX_QL_GLOBAL = intermediate in
+    // global memory (local.cuh); both measured slower than local2.cuh
+    static const bool cluster_local = getenv("VX_QL_CLUSTER") != nullptr;
+    static const bool global_local = getenv("VX_QL_GLOBAL") != nullptr;
+    x.cluster_local = cluster_local;
+    x.global_local = global_local && !cluster_local;
+    const bool q2 = !x.cluster_local && !x.global_local;
+    const uint64_t ql_T = q2 ? Q2Cfg<K, V>::TARGET : QlCfg<K, V>::TARGET;
+    const uint64_t ql_Tmin = q2 ? Q2Cfg<K, V>::TMIN : QlCfg<K, V>::TMIN;
 #ifndef VX_NO_QL
     // the CTA-local level needs leaves of ~2x its bucket target (skipped for a
     // small sort_bound) and enough segments to fill the GPU (one CTA each):
     // below ~256 target-sized segments the finish path alone is faster
-    const bool ql_on = x.leaf >= 2 * QlCfg<K, V>::LT && n >= 256 * QlCfg<K, V>::TARGET;
+    const bool ql_on = x.leaf >= 2 * QlCfg<K, V>::LT && n >= 256 * ql_T;
 #else
     const bool ql_on = false;
 #endif
@@ -547,16 +563,11 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     if (ql_on) {
         // the global levels needed at the full target (leaves up to kQlSlack x
         // target, as qs_plan counts them)
-        const double Lv = ceil(log((double)n / (kQlSlack * (double)QlCfg<K, V>::TARGET)) / log(256.0) - 1e-9);
+        const double Lv = ceil(log((double)n / (kQlSlack * (double)ql_T)) / log(256.0) - 1e-9);
         const double t = (double)n / pow(256.0, Lv < 1.0 ? 1.0 : Lv);
-        x.ql_target =
-            (uint64_t)std::min((double)QlCfg<K, V>::TARGET, std::max((double)QlCfg<K, V>::TMIN, ceil(t)));
+        x.ql_target = (uint64_t)std::min((double)ql_T, std::max((double)ql_Tmin, ceil(t)));
     }
-    // the distributed-shared-memory variant (localc.cuh) is opt-in: measured
-    // slower than the single-CTA level on B200
-    static const bool cluster_local = getenv("VX_QL_CLUSTER") != nullptr;
-    x.cluster_local = cluster_local;
-    x.ql_cap = ql_on ? (x.cluster_local ? QcCfg<K, V>::CAP : QlCfg<K, V>::CAP) : 0;
+    x.ql_cap = ql_on ? (x.cluster_local ? QcCfg<K, V>::CAP : (q2 ? Q2Cfg<K, V>::CAP : QlCfg<K, V>::CAP)) : 0;
     // n <= the finish capacity: the whole array is one finish item whose
     // source is the input
     x.as_fin = n <= L::LOCAL ? 1u : 0u;
@@ -594,8 +605,10 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
             ncl = v;
         }
         x.g_loc = ncl * kQcC;
-    } else {
+    } else if (x.global_local) {
         x.g_loc = x.sms * VX_OCC((qs_local_kernel<K, V>), kQlNT, sizeof(QlSmem<K, V>));
+    } else {
+        x.g_loc = x.sms * VX_OCC((qs_local2_kernel<K, V>), kQlNT, sizeof(Q2Smem<K, V>));
     }
     x.g_seg = 2 * x.sms;
 
@@ -1206,6 +1219,16 @@ int vx_verify(int dtype, const void* keys, const void* values, int64_t n, int ch
     VX_LAUNCHED();
     return VX_OK;
 }
+
+#ifdef VX_QL_PHASES
+// tuning builds only: read and clear the CTA-local level's phase clocks
+int vx_debug_phases(unsigned long long* out) {
+    unsigned long long z[8] = {};
+    VX_CUDA(cudaMemcpyFromSymbol(out, g_ql_phase, sizeof z));
+    VX_CUDA(cudaMemcpyToSymbol(g_ql_phase, z, sizeof z));
+    return VX_OK;
+}
+#endif
 
 // ------------------------------------------------------------ host drop-in
 int vx_host_quicksort(int dtype, void* arr, int64_t n, int64_t lane, int64_t sort_bound, int strategy, int opt_a,
