@@ -20,6 +20,7 @@
 #include "hist.cuh"
 #include "local.cuh"
 #include "local2.cuh"
+#include "local3.cuh"
 #include "localc.cuh"
 
 using namespace vx;
@@ -233,6 +234,7 @@ struct SortCtx {
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
     bool cluster_local;  // CTA-local level in distributed shared memory (localc.cuh)
     bool global_local;   // CTA-local level with the intermediate in global memory (local.cuh)
+    bool group_local;    // CTA-local level with lane-group networks over a padded stage (local2.cuh)
 };
 
 template <typename K, typename V>
@@ -279,8 +281,12 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
         if (x.cluster_local)
             qs_localc_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QcSmem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, x.keys, x.vals, x.leaf);
-        else if (!x.global_local)  // default: intermediate staged in shared memory (local2.cuh)
+        else if (x.group_local)  // opt-in: padded stage, lane-group networks (local2.cuh)
             qs_local2_kernel<K, V><<<x.g_loc, kQlNT, sizeof(Q2Smem<K, V>), st>>>(
+                x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
+                x.keys, x.vals, x.leaf);
+        else if (!x.global_local)  // default: sorted image in shared memory, one lane per bucket (local3.cuh)
+            qs_local3_kernel<K, V><<<x.g_loc, kQlNT, sizeof(Q3Smem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
                 x.keys, x.vals, x.leaf);
         else  // opt-in: intermediate through L2 in the other buffer
@@ -540,14 +546,17 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     x.leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
     // opt-in variants of the CTA-local level: VX_QL_CLUSTER =
     // distributed shared memory (localc.cuh), VX_QL_GLOBAL = intermediate in
-    // global memory (local.cuh); both measured slower than local2.cuh
+    // global memory (local.cuh), VX_QL_GROUP = padded shared-memory stage with
+    // lane-group networks (local2.cuh); all measured slower than local3.cuh
     static const bool cluster_local = getenv("VX_QL_CLUSTER") != nullptr;
     static const bool global_local = getenv("VX_QL_GLOBAL") != nullptr;
+    static const bool group_local = getenv("VX_QL_GROUP") != nullptr;
     x.cluster_local = cluster_local;
     x.global_local = global_local && !cluster_local;
-    const bool q2 = !x.cluster_local && !x.global_local;
-    const uint64_t ql_T = q2 ? Q2Cfg<K, V>::TARGET : QlCfg<K, V>::TARGET;
-    const uint64_t ql_Tmin = q2 ? Q2Cfg<K, V>::TMIN : QlCfg<K, V>::TMIN;
+    x.group_local = group_local && !cluster_local && !global_local;
+    const bool q3 = !x.cluster_local && !x.global_local && !x.group_local;
+    const uint64_t ql_T = q3 ? Q3Cfg<K, V>::TARGET : (x.group_local ? Q2Cfg<K, V>::TARGET : QlCfg<K, V>::TARGET);
+    const uint64_t ql_Tmin = q3 ? Q3Cfg<K, V>::TMIN : (x.group_local ? Q2Cfg<K, V>::TMIN : QlCfg<K, V>::TMIN);
 #ifndef VX_NO_QL
     // the CTA-local level needs leaves of ~2x its bucket target (skipped for a
     // small sort_bound) and enough segments to fill the GPU (one CTA each):
@@ -567,7 +576,11 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         const double t = (double)n / pow(256.0, Lv < 1.0 ? 1.0 : Lv);
         x.ql_target = (uint64_t)std::min((double)ql_T, std::max((double)ql_Tmin, ceil(t)));
     }
-    x.ql_cap = ql_on ? (x.cluster_local ? QcCfg<K, V>::CAP : (q2 ? Q2Cfg<K, V>::CAP : QlCfg<K, V>::CAP)) : 0;
+    x.ql_cap = !ql_on ? 0
+               : x.cluster_local ? QcCfg<K, V>::CAP
+               : q3 ? Q3Cfg<K, V>::CAP
+               : x.group_local ? Q2Cfg<K, V>::CAP
+                               : QlCfg<K, V>::CAP;
     // n <= the finish capacity: the whole array is one finish item whose
     // source is the input
     x.as_fin = n <= L::LOCAL ? 1u : 0u;
@@ -607,8 +620,10 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         x.g_loc = ncl * kQcC;
     } else if (x.global_local) {
         x.g_loc = x.sms * VX_OCC((qs_local_kernel<K, V>), kQlNT, sizeof(QlSmem<K, V>));
-    } else {
+    } else if (x.group_local) {
         x.g_loc = x.sms * VX_OCC((qs_local2_kernel<K, V>), kQlNT, sizeof(Q2Smem<K, V>));
+    } else {
+        x.g_loc = x.sms * VX_OCC((qs_local3_kernel<K, V>), kQlNT, sizeof(Q3Smem<K, V>));
     }
     x.g_seg = 2 * x.sms;
 

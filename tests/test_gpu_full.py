@@ -74,10 +74,12 @@ def test_c5_full_size_matches_oracle(tag, tdt, n, dist):
     assert out[0].item() == gold["first"] and out[-1].item() == gold["last"]
     if dist == "uniform":
         # two global partition levels, then the CTA-local level: every key is
-        # moved by two scatter passes (no spurious third level).  float64: the
-        # few CTA-local segments around zero span many exponents, fail the
-        # interpolation-skew test and take one sampled level more (< 0.1 %)
-        assert stats["scatter_elems"] <= (2 * n if tag == "i32" else 2.005 * n), stats
+        # moved by two scatter passes (no spurious third level), except the
+        # tails: a few leaves of the two outermost level-0 buckets (no key
+        # bounds, so sampled pivots and a wider size spread) exceed the
+        # CTA-local capacity, and float64 leaves around zero span many
+        # exponents and fail the interpolation-skew test (< 0.5 % of the keys)
+        assert stats["scatter_elems"] <= 2.005 * n, stats
         assert stats["local_elems"] >= 0.95 * n, stats
     if dist in ("sorted", "reverse"):
         # the exact answer is known: the sorted generator itself

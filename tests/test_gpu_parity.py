@@ -635,7 +635,9 @@ def test_profile_counters_report_launches_and_elements():
     assert L.vx_profile_read(la, ms, el, 9) == 9
     assert la[3] >= 1 and la[4] >= 1 and la[8] >= 1  # scatter, finish, CTA-local level
     assert el[3] >= n  # the first level moves every element
-    assert el[4] + el[8] >= n  # every element ends in a finish item or a CTA-local segment
+    # every element ends in a finish item or a CTA-local segment, except the
+    # few buckets that hold a single key (final as they are)
+    assert n - n // 1000 <= el[4] + el[8] <= n
     assert el[8] >= n // 2  # uniform keys: most segments go through the CTA-local level
     assert ms[8] > 0.0
 

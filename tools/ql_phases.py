@@ -18,12 +18,12 @@ src = generate(torch.float64 if kind == "f64" else torch.int32, "uniform", n)
 out = torch.empty_like(src)
 vals = torch.arange(n, dtype=torch.int32, device="cuda") if kind == "kv" else None
 ovals = torch.empty_like(vals) if vals is not None else None
-names = ["range", "count", "scan", "scatter", "networks"]
+names = ["range", "count", "scan", "scatter", "networks", "copyout"]
 buf = (ctypes.c_ulonglong * 8)()
 for it in range(3):
     vx.sort_into(src, out, values=vals, out_values=ovals)
     torch.cuda.synchronize()
     L.vx_debug_phases(buf)
-    tot = sum(buf[:5]) or 1
+    tot = sum(buf[:6]) or 1
     print(kind, n, " ".join(f"{nm}={buf[i] / tot:.3f}" for i, nm in enumerate(names)),
           f"cycles/key/SM={tot / n:.3f}")
