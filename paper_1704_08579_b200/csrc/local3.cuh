@@ -32,6 +32,7 @@
 #include "local.cuh"
 #include "local2.cuh"
 #include "qsort.cuh"
+#include "tma.cuh"
 
 namespace vx {
 
@@ -175,6 +176,30 @@ __device__ __forceinline__ void image_copy_out(const T* img, T* __restrict__ dst
     if (t0 + threadIdx.x < n) dst[t0 + threadIdx.x] = img[t0 + threadIdx.x];
 }
 
+// The same, with the aligned body as ONE thread's bulk stores (TMA), which
+// drain while the CTA goes on to the next leaf: the caller fences the async
+// proxy + barriers before, and waits for the reads (bulk_wait_read) before
+// the image is overwritten.
+template <typename T, unsigned NT>
+__device__ __forceinline__ void image_store_async(const T* img, T* __restrict__ dst, unsigned n) {
+    constexpr unsigned VE = 16 / sizeof(T);
+    if (((reinterpret_cast<uintptr_t>(img) ^ reinterpret_cast<uintptr_t>(dst)) & 15) != 0) {
+        for (unsigned i = threadIdx.x; i < n; i += NT) dst[i] = img[i];
+        return;
+    }
+    const unsigned head = min(n, (unsigned)(((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) / sizeof(T)));
+    const unsigned nv = (n - head) / VE;
+    if (threadIdx.x == 0) {
+        constexpr unsigned CH = 32768;  // bytes per bulk store
+        const char* s = reinterpret_cast<const char*>(img + head);
+        char* d = reinterpret_cast<char*>(dst + head);
+        for (unsigned o = 0; o < nv * 16; o += CH) bulk_s2g(d + o, s + o, min(CH, nv * 16 - o));
+    }
+    if (threadIdx.x >= 32 && threadIdx.x < 32 + head) dst[threadIdx.x - 32] = img[threadIdx.x - 32];
+    const unsigned t0 = head + nv * VE;
+    if (threadIdx.x >= 64 && t0 + threadIdx.x - 64 < n) dst[t0 + threadIdx.x - 64] = img[t0 + threadIdx.x - 64];
+}
+
 template <typename K, typename V>
 __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
                                                              Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
@@ -311,26 +336,6 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
         const unsigned ex0 = block_excl_scan<NT>(sum, sm.scan, &tot);  // tot == len
         const unsigned G = tot <= C::SCAP ? 1u : (tot + (C::SCAP - 256) - 1) / (C::SCAP - 256);
         const unsigned W = G == 1 ? 0xffffffffu : (tot + G - 1) / G;
-        if (tid < nbt) {
-            // a bucket opens a group when its offset enters the group's window
-            unsigned ex = ex0;
-            unsigned prevo = tid > 0 ? ex0 - sm.tab[tid * BPT - 1] : 0u;
-#pragma unroll
-            for (unsigned q = 0; q < BPT; ++q) {
-                const unsigned b = tid * BPT + q;
-                if (b < nb && (b == 0 || prevo / W != ex / W)) {
-                    sm.gstart[ex / W] = ex;
-                    sm.gfirst[ex / W] = b;
-                }
-                prevo = ex;
-                ex += c[q];
-            }
-        }
-        if (tid == 0) {
-            sm.gstart[G] = tot;
-            sm.gfirst[G] = nb;
-        }
-        __syncthreads();
         // a leaf sorted in place in G > 1 groups: the groups before the last
         // still have readers of the source, so their images detour through
         // the other buffer and come home after the last group's pass
@@ -340,15 +345,55 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
             const K* d = (detour && g + 1 < G ? oth_k : out_k) + start + gs;
             return (unsigned)((reinterpret_cast<uintptr_t>(d) & 15) / sizeof(K));
         };
-        if (tid < nbt) {
-            unsigned ex = ex0;
+        if (G == 1) {
+            if (tid < nbt) {
+                unsigned ex = ex0 + phase_of(0, 0);
 #pragma unroll
-            for (unsigned q = 0; q < BPT; ++q) {
-                const unsigned g = ex / W, gs = sm.gstart[g];
-                sm.tab[tid * BPT + q] = ((ex - gs + phase_of(g, gs)) << 16) | c[q];
-                ex += c[q];
+                for (unsigned q = 0; q < BPT; ++q) {
+                    sm.tab[tid * BPT + q] = (ex << 16) | c[q];
+                    ex += c[q];
+                }
+            }
+            if (tid == 0) {
+                sm.gstart[0] = 0;
+                sm.gfirst[0] = 0;
+                sm.gstart[1] = tot;
+                sm.gfirst[1] = nb;
+            }
+        } else {
+            if (tid < nbt) {
+                // a bucket opens a group when its offset enters the group's window
+                unsigned ex = ex0;
+                unsigned prevo = tid > 0 ? ex0 - sm.tab[tid * BPT - 1] : 0u;
+#pragma unroll
+                for (unsigned q = 0; q < BPT; ++q) {
+                    const unsigned b = tid * BPT + q;
+                    if (b < nb && (b == 0 || prevo / W != ex / W)) {
+                        sm.gstart[ex / W] = ex;
+                        sm.gfirst[ex / W] = b;
+                    }
+                    prevo = ex;
+                    ex += c[q];
+                }
+            }
+            if (tid == 0) {
+                sm.gstart[G] = tot;
+                sm.gfirst[G] = nb;
+            }
+            __syncthreads();
+            if (tid < nbt) {
+                unsigned ex = ex0;
+#pragma unroll
+                for (unsigned q = 0; q < BPT; ++q) {
+                    const unsigned g = ex / W, gs = sm.gstart[g];
+                    sm.tab[tid * BPT + q] = ((ex - gs + phase_of(g, gs)) << 16) | c[q];
+                    ex += c[q];
+                }
             }
         }
+        // the previous leaf's image has left shared memory before anything
+        // overwrites it
+        if (tid == 0) bulk_wait_read();
         __syncthreads();
         VX_QL_TICK(2);
         for (unsigned g = 0; g < G; ++g) {
@@ -418,15 +463,22 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
                                           __shfl_sync(0xffffffffu, cb, src));
                 }
             }
+            if (G == 1) fence_async_smem();
             __syncthreads();
             VX_QL_TICK(4);
             // ---- 5. the image to the output
-            {
+            if (G == 1) {
+                image_store_async<K, NT>(sm.k + ph, out_k + start, glen);
+                if constexpr (KV) image_store_async<V, NT>(stv + ph, out_v + start, glen);
+                if (tid == 0) bulk_commit();
+                // (no barrier: the next leaf's range / count / scan passes do
+                // not touch the image; its scan waits for the store's reads)
+            } else {
                 const bool away = detour && g + 1 < G;
                 image_copy_out<K, NT>(sm.k + ph, (away ? oth_k : out_k) + start + gs, glen);
                 if constexpr (KV) image_copy_out<V, NT>(stv + ph, (away ? oth_v : out_v) + start + gs, glen);
+                __syncthreads();
             }
-            __syncthreads();
             VX_QL_TICK(5);
         }
         if (detour) {
@@ -439,6 +491,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
         }
         done += len;
     }
+    if (tid == 0) bulk_wait_read();  // the last image is still being read
     if (tid == 0 && done) atomicAdd(&ctl->loc_elems, done);
 }
 

@@ -56,6 +56,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
         : "memory");
 }
 
+// shared -> global bulk store (bulk async-group completion).  src / dst are
+// 16-byte aligned, bytes a multiple of 16.  The threads that wrote the source
+// fence the async proxy (fence_async_smem) before the barrier that precedes
+// the issue; the issuing thread commits, and waits for the group's smem READS
+// before the source is overwritten.
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
+                 "r"(smem_u32(src_smem)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
 // Metadata of one staged tile.
 struct BulkTile {
     uint64_t base;  // first element (absolute index)
