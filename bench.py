@@ -35,6 +35,7 @@ import argparse
 import ctypes
 import json
 import os
+import re
 import shutil
 import statistics
 import subprocess
@@ -208,7 +209,12 @@ def ncu_traffic(workload, kernel_class):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        e = d.get(workload, {}).get(KERNEL_REGEX.get(kernel_class, kernel_class))
+        name = KERNEL_REGEX.get(kernel_class, kernel_class)
+        w = d.get(workload, {})
+        e = w.get(name)
+        if e is None and kernel_class == "qs_local":  # the CTA-local level's kernel variants (local*.cuh)
+            e = next((v for k, v in w.items() if re.fullmatch(r"qs_local\w*_kernel", k) and v["bytes_per_launch"] > 1e6),
+                     None)
         return None if e is None else round(e["bytes_per_launch"])
     except Exception:
         return None

@@ -7,11 +7,31 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace vx {
 
 constexpr int kWarp = 32;
+
+// Checked build (-DVX_CHECK; tools/check_build.sh): device-side assertions on
+// every bucket index, staging slot and destination index of the kernels.  A
+// failed assertion traps, which fails the launch and every test after it.
+// (compute-sanitizer is closed on this GPU pool; these bounds checks plus
+// the canary tests stand in for memcheck.)
+#ifdef VX_CHECK
+#define VX_ASSERT(cond)                                                    \
+    do {                                                                   \
+        if (!(cond)) {                                                     \
+            printf("VX_ASSERT failed: %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+            __trap();                                                      \
+        }                                                                  \
+    } while (0)
+#else
+#define VX_ASSERT(cond) \
+    do {                \
+    } while (0)
+#endif
 
 template <typename K>
 struct KeyTraits;

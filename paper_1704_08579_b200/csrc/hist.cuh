@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 const unsigned b = classify(sb[i * kQsNT + tid]);
+                VX_ASSERT(b < nb && bt.base + i * kQsNT + tid < n_all);
                 // result unused: ATOMS.POPC.INC, which already merges the
                 // lanes of a warp that hit one counter (sorted inputs)
                 atomicAdd(&s_hist[b], 1u);
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                 if (idx < bt.tn) {
                     const K x = tile_get<K>(buf, bt, src, idx);
                     const unsigned b = classify(x);
+                    VX_ASSERT(b < nb && bt.base + idx < n_all);
                     atomicAdd(&s_hist[b], 1u);
                     ids[bt.base + idx] = (unsigned short)b;
                 }

@@ -287,11 +287,11 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
             } else {
                 u = OKey<K>::of(key);
             }
-#ifdef VX_CHECK
-            if (u < lo || u > hi) __trap();
-#endif
+            VX_ASSERT(u >= lo && u <= hi);  // every key lies inside the leaf's bounds
             const uint32_t d = (uint32_t)((u - lo) >> sh);
-            return mul ? __umulhi(d, mul) : d;
+            const unsigned bk = mul ? __umulhi(d, mul) : d;
+            VX_ASSERT(bk < nb);
+            return bk;
         };
         const unsigned nbt = (nb + BPT - 1) / BPT;  // threads that own buckets
         if (tid < nbt) {
@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
         }
         unsigned tot;
         const unsigned ex0 = block_excl_scan<NT>(sum, sm.scan, &tot);  // tot == len
+        VX_ASSERT(tot == len);
         const unsigned G = tot <= C::SCAP ? 1u : (tot + (C::SCAP - 256) - 1) / (C::SCAP - 256);
         const unsigned W = G == 1 ? 0xffffffffu : (tot + G - 1) / G;
         // a leaf sorted in place in G > 1 groups: the groups before the last
@@ -368,9 +369,11 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
 #pragma unroll
                 for (unsigned q = 0; q < BPT; ++q) {
                     const unsigned b = tid * BPT + q;
-                    if (b < nb && (b == 0 || prevo / W != ex / W)) {
-                        sm.gstart[ex / W] = ex;
-                        sm.gfirst[ex / W] = b;
+                    // (empty buckets at the very end, offset == tot == G * W, stay in the last group)
+                    const unsigned gq = min(ex / W, G - 1), gp = min(prevo / W, G - 1);
+                    if (b < nb && (b == 0 || gp != gq)) {
+                        sm.gstart[gq] = ex;
+                        sm.gfirst[gq] = b;
                     }
                     prevo = ex;
                     ex += c[q];
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
                 unsigned ex = ex0;
 #pragma unroll
                 for (unsigned q = 0; q < BPT; ++q) {
-                    const unsigned g = ex / W, gs = sm.gstart[g];
+                    const unsigned g = min(ex / W, G - 1), gs = sm.gstart[g];
                     sm.tab[tid * BPT + q] = ((ex - gs + phase_of(g, gs)) << 16) | c[q];
                     ex += c[q];
                 }
@@ -406,13 +409,16 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
             if (G == 1) {
                 if constexpr (!KV) {
                     seg_for_each<K, NT>(sk, len, [&](K x) {
-                        sm.k[atomicAdd(&sm.tab[bucket(x)], 0x10000u) >> 16] = x;
+                        const unsigned p = atomicAdd(&sm.tab[bucket(x)], 0x10000u) >> 16;
+                        VX_ASSERT(p >= ph && p < ph + glen);
+                        sm.k[p] = x;
                     });
                 } else {
                     const V* svp = src_v + start;
                     seg_for_each_idx<K, NT>(sk, len, [&](K x, unsigned i) {
                         const V y = svp[i];
                         const unsigned p = atomicAdd(&sm.tab[bucket(x)], 0x10000u) >> 16;
+                        VX_ASSERT(p >= ph && p < ph + glen);
                         sm.k[p] = x;
                         stv[p] = y;
                     });
@@ -423,6 +429,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
                     const unsigned b = bucket(x);
                     if (b - b_lo < nbg) {
                         const unsigned p = atomicAdd(&sm.tab[b], 0x10000u) >> 16;
+                        VX_ASSERT(p >= ph && p < ph + glen);
                         sm.k[p] = x;
                         if constexpr (KV) stv[p] = svp[i];
                     }
@@ -451,6 +458,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
                     const unsigned t = sm.tab[b];  // the cursor ended at the bucket's end
                     cb = t & 0xffffu;
                     ps = (t >> 16) - cb;
+                    VX_ASSERT(ps >= ph && ps + cb <= ph + glen && ph + glen + C::TAIL <= C::SLOTS);
                 }
                 const bool big = cb > (unsigned)LE;
                 lane_sort<K, V, LE>(sm.k, stv, ps, big ? 0u : cb);

@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(NT) partition2_kernel(const K* __restrict__ ki
     const uint64_t hi_base = n - H_excl - H_t;
     for (unsigned j = tid; j < N_t; j += NT) {
         const uint64_t dst = j < L_t ? L_excl + j : hi_base + (j - L_t);
+        VX_ASSERT(dst < n);
         kout[dst] = sk[j];
         if constexpr (KV) vout[dst] = sv[j];
     }

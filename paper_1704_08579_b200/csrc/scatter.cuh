@@ -25,6 +25,9 @@ struct ScatterPipeSmem {
         unsigned short b[TILE];
         unsigned long long delta[kMaxBkt + 1];  // destination of slot j in bucket b: delta[b] + j
         unsigned tn;
+#ifdef VX_CHECK
+        unsigned long long lo, hi;  // the owning segment's range in the destination
+#endif
     };
     Stage st[2];
     unsigned cnt[2][kMaxBkt + 1];  // per-tile counts, then (in place) bucket offsets; double-buffered
@@ -36,6 +39,7 @@ __device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K,
     constexpr bool KV = HasVal<V>::value;
     for (unsigned j = threadIdx.x; j < s.tn; j += kQsNT) {
         const unsigned long long pos = s.delta[s.b[j]] + j;
+        VX_ASSERT(pos >= s.lo && pos < s.hi);  // inside the tile's segment
         dst_k[pos] = s.k[j];
         if constexpr (KV) dst_v[pos] = s.v[j];
     }
@@ -127,6 +131,12 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         if (b0 < nb) cnt[b0] = ex;
         if (b1 < nb) cnt[b1] = ex + c0;
         if (threadIdx.x == 0) S.tn = g.tn;
+#ifdef VX_CHECK
+        if (threadIdx.x == 0) {
+            S.lo = segs[g.seg].start;
+            S.hi = segs[g.seg].start + segs[g.seg].len;
+        }
+#endif
         // overlap: write out the previous tile while the reservations fly
         if (t > t0) stage_writeout<K, V>(sm.st[p ^ 1], dst_k, dst_v);
         if (c0) S.delta[b0] = r0 - ex;
@@ -138,6 +148,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
 #pragma unroll
             for (int i = 0; i < IPT; ++i) {
                 const unsigned slot = cnt[br[i] >> 16] + (br[i] & 0xffffu);
+                VX_ASSERT(slot < (unsigned)TILE && (br[i] >> 16) < nb);
                 S.k[slot] = k[i];
                 if constexpr (KV) S.v[slot] = v[i];
                 S.b[slot] = (unsigned short)(br[i] >> 16);
@@ -147,6 +158,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
             for (int i = 0; i < IPT; ++i) {
                 if (br[i] != 0xffffffffu) {
                     const unsigned slot = cnt[br[i] >> 16] + (br[i] & 0xffffu);
+                    VX_ASSERT(slot < g.tn && (br[i] >> 16) < nb);
                     S.k[slot] = k[i];
                     if constexpr (KV) S.v[slot] = v[i];
                     S.b[slot] = (unsigned short)(br[i] >> 16);

@@ -71,6 +71,24 @@ def full_rows(rep):
     return res
 
 
+def traffic_rows(rep):
+    """(kernel, ms, dram bytes) per launch of a report that holds only
+    gpu__time_duration.sum and the two dram__bytes metrics (the 2^32 / 2^31
+    headline steps: a --set full capture replays every 16 GiB launch ~40x)."""
+    m = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"]
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics", ",".join(m)],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        u = dict(zip(hdr, units))
+        res.append({"kernel": short(d["Kernel Name"]), "ms": to_ms(d[m[0]], u[m[0]]),
+                    "dram_read": to_bytes(d[m[1]], u[m[1]]), "dram_write": to_bytes(d[m[2]], u[m[2]])})
+    return res
+
+
 def launch_rows(path):
     txt = open(path).read()
     i = txt.find('"ID"')
@@ -92,6 +110,7 @@ def launch_rows(path):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", nargs="*", default=[])
+    ap.add_argument("--traffic", nargs="*", default=[], help="REP:WORKLOAD reports with time + DRAM bytes only")
     ap.add_argument("--launches", default=None)
     ap.add_argument("--tag", default="r1")
     ap.add_argument("--note", default="")
@@ -125,6 +144,28 @@ def main():
             if wl:
                 traffic[wl] = {k: {"bytes_per_launch": v[1] / v[0], "launches": v[0], "ms_per_launch": v[2] / v[0]}
                                for k, v in acc.items()}
+        lines.append("")
+    if a.traffic:
+        lines += ["## DRAM bytes per launch of the headline steps (`--metrics gpu__time_duration.sum,"
+                  "dram__bytes_read.sum,dram__bytes_write.sum`)", "",
+                  "| workload | kernel | launches | ms / launch | DRAM read GB / launch | DRAM write GB / launch | DRAM GB/s "
+                  "| % of HBM peak |", "|---|---|---|---|---|---|---|---|"]
+        for spec in a.traffic:
+            rep, _, wl = spec.partition(":")
+            acc = collections.OrderedDict()
+            for r in traffic_rows(rep):
+                base = r["kernel"].split("<")[0]
+                a_ = acc.setdefault(base, [0, 0.0, 0.0, 0.0])
+                a_[0] += 1
+                a_[1] += r["dram_read"]
+                a_[2] += r["dram_write"]
+                a_[3] += r["ms"]
+            for k, v in acc.items():
+                gbs = (v[1] + v[2]) / (v[3] * 1e-3) / 1e9 if v[3] else 0
+                lines.append(f"| {wl} | `{k}` | {v[0]} | {v[3]/v[0]:.3f} | {v[1]/v[0]/1e9:.3f} | {v[2]/v[0]/1e9:.3f} | "
+                             f"{gbs:.0f} | {100*gbs/peak:.1f} |")
+            traffic[wl] = {k: {"bytes_per_launch": (v[1] + v[2]) / v[0], "launches": v[0], "ms_per_launch": v[3] / v[0]}
+                           for k, v in acc.items()}
         lines.append("")
     if a.launches:
         agg = launch_rows(a.launches)
