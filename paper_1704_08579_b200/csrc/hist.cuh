@@ -87,12 +87,17 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     __syncthreads();
 
     unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, rsh = 0;
-    bool radix = false;
+    bool radix = false, vmode = false;
     U rlo = 0;
+    double vlo = 0.0, vinv = 0.0;
     CellParams<U> cp{};
     // equal-width segments: bucket = umulhi(code - lo, mul) (keys lie in
     // [lo, hi] by construction, so the bucket is < nb)
     auto classify = [&](K key) -> unsigned {
+        if constexpr (sizeof(K) == 8) {
+            // value-space equal-width buckets (mode 2)
+            if (vmode) return min(nb - 1, (unsigned)__double2uint_rz(((double)key - vlo) * vinv));
+        }
         if (radix) {
             const uint32_t d = (uint32_t)(OKey<K>::of(key) - rlo);
             return min(nb - 1, rsh ? __umulhi(d, rsh) : d);
@@ -120,9 +125,12 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             bkt_off = sg.bkt_off;
             nb = sg.nb;
             radix = sg.mode == 1;
+            vmode = sg.mode == 2;
+            vlo = sg.vlo;
+            vinv = sg.vinv;
             rlo = (U)sg.lo;
             rsh = sg.mul;
-            if (!radix) cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
+            if (!radix && !vmode) cp = ct_load<K, kQsNT>(s_ct, spl_pool, sg.spl_off, sg.m, s_scan);  // barriers inside
             for (unsigned b = tid; b < nb; b += kQsNT) s_hist[b] = 0;
             __syncthreads();
         }

@@ -43,7 +43,7 @@ namespace vx {
 #define VX_Q3_TARGET_BYTES (150 * 1024)
 #endif
 #ifndef VX_Q3_TARGET8_BYTES
-#define VX_Q3_TARGET8_BYTES (256 * 1024)
+#define VX_Q3_TARGET8_BYTES (150 * 1024)
 #endif
 #ifndef VX_Q3_TMIN_BYTES
 #define VX_Q3_TMIN_BYTES (96 * 1024)
@@ -64,10 +64,10 @@ struct Q3Cfg {
     static constexpr unsigned TAIL = 256 + 16;  // sentinel slots after the image (the widest network + alignment)
     static constexpr unsigned SLOTS = VX_Q3_STAGE_BYTES / BYTES;
     static constexpr unsigned SCAP = SLOTS - TAIL - 16;  // largest image
-    // the plan aims the leaves here (at most).  4-byte keys reach it at any
-    // n <= 2^32 (a sampled level of 256 buckets, then an equal-width level of
-    // up to 511), just below 4 rounds of buckets; 8-byte keys have sampled
-    // levels only (256 x 256): two groups per leaf at n = 2^31
+    // the plan aims the leaves here (at most): reached at any n <= 2^32 by a
+    // sampled level of 256 buckets, then an equal-width level of up to 511
+    // (code space for 4-byte keys, value space for float64); just below 4
+    // rounds of buckets for 4-byte keys
     static constexpr uint64_t TARGET = (sizeof(K) == 4 ? VX_Q3_TARGET_BYTES : VX_Q3_TARGET8_BYTES) / BYTES;
     static constexpr uint64_t TMIN = VX_Q3_TMIN_BYTES / BYTES;
     static constexpr uint64_t CAPB = (uint64_t)(NB - ROUND) * LT10 / 10;

@@ -77,11 +77,15 @@ struct FinCap {
 // equal-width buckets over [lo, hi], bucket = umulhi(code - lo, mul) with
 // mul = floor(nb * 2^32 / (hi - lo + 1)) -- evenly spaced pivots, classified
 // with a subtract and a high multiply (mul = 0: one code per bucket).
+// mode 2 (the same for float64 keys): nb equal-width buckets in VALUE space,
+// bucket = min(nb - 1, trunc((x - vlo) * vinv)) -- float64 codes change
+// density at every binade, values of locally uniform keys do not.
 struct Seg {
     unsigned long long start, len;
     unsigned spl_off, m, bkt_off, tile_base;
     unsigned long long lo, hi;  // key-code bounds (lo > hi: unknown)
     unsigned nb, shift, mode, mul;
+    double vlo, vinv;  // mode 2
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -580,10 +584,10 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         const uint64_t start = segs[s].start, len = segs[s].len;
         using U = typename OKey<K>::U;
         const uint64_t slo = segs[s].lo, shi = segs[s].hi;
-        // 4-byte keys only: float64 codes change density at every binade,
-        // which unbalances equal-width buckets (measured slower)
+        // bounds known from the parent: equal-width buckets, in code space
+        // for 4-byte keys and in value space for float64
 #ifndef VX_NO_RADIX
-        const bool radix = sizeof(K) == 4 && slo < shi;
+        const bool radix = slo < shi;
 #else
         const bool radix = false;
 #endif
@@ -616,8 +620,16 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             const uint64_t range = (uint64_t)(U)(shi - slo);
             unsigned nb = rb;
             unsigned mul = 0;
-            if (range + 1 <= (uint64_t)nb) nb = (unsigned)(range + 1);  // one code per bucket
-            else mul = (unsigned)(((uint64_t)nb << 32) / (range + 1));
+            double vlo = 0.0, vinv = 0.0;
+            if constexpr (sizeof(K) == 4) {
+                if (range + 1 <= (uint64_t)nb) nb = (unsigned)(range + 1);  // one code per bucket
+                else mul = (unsigned)(((uint64_t)nb << 32) / (range + 1));
+            } else {
+                // value space: x in [vlo, vhi] -> trunc((x - vlo) * vinv) in [0, nb)
+                vlo = ord_to_f64((uint64_t)slo);
+                const double w = ord_to_f64((uint64_t)shi) - vlo;  // > 0 (slo < shi; -0.0 / +0.0 aside)
+                vinv = w > 0.0 && w < 1.7e308 ? (double)nb * (1.0 - 1e-12) / w : 0.0;  // 0: everything in bucket 0
+            }
             if (threadIdx.x == 0) {
                 const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
                 unsigned bo = atomicAdd(&ctl->bkt_ctr, nb);
@@ -637,7 +649,9 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 segs[s].nb = nb;
                 segs[s].shift = 0;
                 segs[s].mul = mul;
-                segs[s].mode = 1;
+                segs[s].mode = sizeof(K) == 4 ? 1 : 2;
+                segs[s].vlo = vlo;
+                segs[s].vinv = vinv;
             }
             __syncthreads();
             for (unsigned b = threadIdx.x; b < nb; b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
@@ -774,7 +788,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
     for (unsigned s = blockIdx.x; s < nseg; s += gridDim.x) {
         const Seg sg = segs[s];
         const unsigned nb = sg.nb;
-        const bool radix = sg.mode == 1;
+        const bool radix = sg.mode != 0;
         const unsigned b = threadIdx.x;
         const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + b] : 0ull;
         const unsigned long long ex = block_excl_scan_u64<kPlanNT>(c, s_scan);
@@ -787,7 +801,30 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
             // more than half its parent is skewed: it forgets its bounds
             // and is partitioned around sampled pivots.
             unsigned long long clo = 1, chi = 0;
-            if (radix) {
+            if (sg.mode == 2) {
+                // value-space bucket b holds x with trunc((x - vlo) * vinv) == b:
+                // bounds widened by 1/1000 of a bucket against rounding, kept
+                // inside the parent's; a bucket too narrow for that margin to
+                // dominate the rounding of vlo + offset leaves them unknown
+                if constexpr (sizeof(K) == 8) {
+                    if (sg.vinv > 0.0) {
+                        const double w = 1.0 / sg.vinv;  // bucket width
+                        const double lo_v = sg.vlo + ((double)b - 1e-3) * w, hi_v = sg.vlo + ((double)b + 1.001) * w;
+                        const double mag = fmax(fabs(lo_v), fabs(hi_v));
+                        if (w * 1e-3 > mag * 1e-15) {
+                            const unsigned long long cl = f64_to_ord(lo_v), ch = f64_to_ord(hi_v);
+                            clo = cl > sg.lo ? cl : sg.lo;
+                            chi = ch < sg.hi ? ch : sg.hi;
+                            if (b == 0) clo = sg.lo;
+                            if (b + 1 == nb) chi = sg.hi;
+                        }
+                    }
+                }
+                if (2 * c > sg.len) {
+                    clo = 1;
+                    chi = 0;
+                }
+            } else if (radix) {
                 // bucket b holds the offsets d with umulhi(d, mul) == b:
                 // [ceil(b * 2^32 / mul), ceil((b + 1) * 2^32 / mul) - 1]
                 auto dlo = [&](unsigned long long bb) -> unsigned long long {
@@ -805,7 +842,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                 chi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
             }
             if (c > 0) {
-                const bool final_ = c == 1 || (radix ? (sg.mul == 0) : (b & 1u) != 0);
+                const bool final_ = c == 1 || (sg.mode == 1 ? (sg.mul == 0) : sg.mode == 0 && (b & 1u) != 0);
                 if (final_) {
                     if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
                         const unsigned nch = (unsigned)((c + kCopyChunk - 1) / kCopyChunk);
