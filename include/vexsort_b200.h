@@ -63,9 +63,19 @@ typedef struct {
     int32_t pivot_strategy;
     int32_t skip_empty_stores;
     int32_t swap_buffered;
-    int32_t reserved;
+    int32_t flags; /* VX_SORT_* bits (0 = default) */
     uint64_t pivot_seed;
 } vx_sort_config;
+
+/* vx_sort_config.flags.  A sort normally runs its level loop from the host
+ * (one 64-byte status read per partition level) the first few times it sees
+ * a set of buffers, and replays a cached CUDA graph -- no host
+ * synchronisation at all -- once the same buffers keep coming back;
+ * VX_SORT_GRAPH builds the graph on the first call (steady-state loops),
+ * VX_SORT_EAGER never builds one.  Inside a caller's stream capture the sort
+ * always records itself into the caller's graph. */
+#define VX_SORT_GRAPH 1
+#define VX_SORT_EAGER 2
 
 const char *vx_last_error(void);
 int vx_version(void);

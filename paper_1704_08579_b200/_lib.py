@@ -15,6 +15,7 @@ import threading
 __all__ = ["BackendUnavailable", "lib", "check", "lib_path", "VX_I32", "VX_F64", "SortConfigC", "SortStatsC"]
 
 VX_I32, VX_F64 = 0, 1
+VX_SORT_GRAPH, VX_SORT_EAGER = 1, 2  # vx_sort_config.flags
 _HERE = os.path.dirname(os.path.abspath(__file__))
 # VEXSORT_B200_LIB overrides the library path (tuning experiments only)
 _SO = os.environ.get("VEXSORT_B200_LIB") or os.path.join(_HERE, "libvexsort_b200.so")
@@ -30,7 +31,7 @@ class SortConfigC(ctypes.Structure):
         ("pivot_strategy", ctypes.c_int32),
         ("skip_empty_stores", ctypes.c_int32),
         ("swap_buffered", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
         ("pivot_seed", ctypes.c_uint64),
     ]
 

@@ -12,7 +12,7 @@ from __future__ import annotations
 import ctypes
 from dataclasses import dataclass
 
-from ._lib import SortConfigC, SortStatsC, check, lib
+from ._lib import VX_SORT_GRAPH, SortConfigC, SortStatsC, check, lib
 from ._region import check_kv, check_region, dev_ptr, host_ptr, on_device, stream_of, workspace
 from .lanes import get_backend, is_device
 
@@ -76,9 +76,9 @@ def select_pivot(region, lo: int, hi: int, strategy: str = "median3", lcg_state:
     return hi
 
 
-def _cfg(config: SortConfig, bound: int) -> SortConfigC:
+def _cfg(config: SortConfig, bound: int, flags: int = 0) -> SortConfigC:
     return SortConfigC(bound, _PIVOT_STRATEGIES.index(config.pivot_strategy), int(config.skip_empty_stores),
-                       int(config.swap_buffered), 0, int(config.pivot_seed) & _U64)
+                       int(config.swap_buffered), flags, int(config.pivot_seed) & _U64)
 
 
 def sort_with_config(region, config: SortConfig) -> None:
@@ -105,7 +105,8 @@ def _device_sort(kind, src, values, out, out_values, config, bound, check_status
     n = len(src)
     with on_device(src):
         ws = workspace(L.vx_sort_workspace_bytes(kind.code, int(values is not None), n), src.device)
-        cfg = _cfg(config, bound)
+        # a call that promises no host synchronisation replays a CUDA graph from the first call on
+        cfg = _cfg(config, bound, VX_SORT_GRAPH if not check_status and stats is None else 0)
         st = stream_of(src)
         check(L.vx_sort_into(kind.code, dev_ptr(src), dev_ptr(values) if values is not None else None,
                              dev_ptr(out), dev_ptr(out_values) if out_values is not None else None, n,
