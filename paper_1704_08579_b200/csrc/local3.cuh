@@ -120,6 +120,37 @@ __device__ __forceinline__ void lane_sort(K* sk, V* sv, unsigned ps, unsigned cb
     }
 }
 
+// int32 keys with a payload, in a leaf whose key codes span less than 2^27:
+// the lane sorts ONE word per pair, (code - lo) << 4 | slot, with the
+// keys-only network (min / max instead of a compare and four selects per
+// comparator), then fetches each pair's payload from the slot the word
+// names.  Equal keys come out in slot order (any order is allowed).
+template <typename K, typename V, int E>
+__device__ __forceinline__ void lane_sort_packed(K* sk, V* sv, unsigned ps, unsigned cb, uint32_t lo) {
+    static_assert(E == 16 && sizeof(K) == 4, "4 slot bits next to a 27-bit key offset");
+    const unsigned lane = threadIdx.x & 31;
+    int32_t w[E];
+    NoVal nv[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const unsigned q = (r + lane) & (E - 1);
+        const uint32_t d = min(OKey<K>::of(sk[ps + q]) - lo, 0x07ffffffu);  // (the sentinel tail saturates)
+        w[r] = (int32_t)((d << 4) | q);
+    }
+    WarpBitonic<int32_t, NoVal, E, 1, true>::sort(w, nv);
+    V val[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r)
+        if (r < (int)cb) val[r] = sv[ps + ((unsigned)w[r] & 15u)];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        if (r < (int)cb) {
+            sk[ps + r] = (K)((((uint32_t)w[r] >> 4) + lo) ^ 0x80000000u);
+            sv[ps + r] = val[r];
+        }
+    }
+}
+
 // A bucket of cb <= 32 * E keys through the whole warp's shuffle network, in
 // place in the image (later buckets' keys pad it, as above).
 template <typename K, typename V, int E>
@@ -461,7 +492,12 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
                     VX_ASSERT(ps >= ph && ps + cb <= ph + glen && ph + glen + C::TAIL <= C::SLOTS);
                 }
                 const bool big = cb > (unsigned)LE;
-                lane_sort<K, V, LE>(sm.k, stv, ps, big ? 0u : cb);
+                if constexpr (KV && sizeof(K) == 4 && LE == 16) {
+                    if (range < 0x07ffffffu) lane_sort_packed<K, V, LE>(sm.k, stv, ps, big ? 0u : cb, (uint32_t)lo);
+                    else lane_sort<K, V, LE>(sm.k, stv, ps, big ? 0u : cb);
+                } else {
+                    lane_sort<K, V, LE>(sm.k, stv, ps, big ? 0u : cb);
+                }
                 // the few buckets above a lane's slots take the whole warp
                 unsigned bm = __ballot_sync(0xffffffffu, big);
                 while (bm) {
