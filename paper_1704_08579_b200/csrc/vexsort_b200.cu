@@ -21,7 +21,6 @@
 #include "local.cuh"
 #include "local2.cuh"
 #include "local3.cuh"
-#include "localc.cuh"
 
 using namespace vx;
 
@@ -232,7 +231,6 @@ struct SortCtx {
     uint64_t n, seed, ql_target, ql_cap;
     unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags, strategy, flags;
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
-    bool cluster_local;  // CTA-local level in distributed shared memory (localc.cuh)
     bool global_local;   // CTA-local level with the intermediate in global memory (local.cuh)
     bool group_local;    // CTA-local level with lane-group networks over a padded stage (local2.cuh)
 };
@@ -283,10 +281,7 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
     if (x.ql_cap) {
         // medium children: CTA-local last level + leaves (data in dst)
         Launch l(KC_LOCAL, st, timed ? 1 : 0, timed);
-        if (x.cluster_local)
-            qs_localc_kernel<K, V><<<x.g_loc, kQlNT, sizeof(QcSmem<K, V>), st>>>(
-                x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, x.keys, x.vals, x.leaf);
-        else if (x.group_local)  // opt-in: padded stage, lane-group networks (local2.cuh)
+        if (x.group_local)  // opt-in: padded stage, lane-group networks (local2.cuh)
             qs_local2_kernel<K, V><<<x.g_loc, kQlNT, sizeof(Q2Smem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
                 x.keys, x.vals, x.leaf);
@@ -578,17 +573,15 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     // the bitonic leaf bound: the reference's sort_bound when given, else
     // the widest warp network (kWarpSortMax = 256); see DESIGN.md
     x.leaf = (cfg && cfg->sort_bound > 0) ? (unsigned)bound : kWarpSortMax;
-    // opt-in variants of the CTA-local level: VX_QL_CLUSTER =
-    // distributed shared memory (localc.cuh), VX_QL_GLOBAL = intermediate in
-    // global memory (local.cuh), VX_QL_GROUP = padded shared-memory stage with
-    // lane-group networks (local2.cuh); all measured slower than local3.cuh
-    static const bool cluster_local = getenv("VX_QL_CLUSTER") != nullptr;
+    // opt-in predecessors of the CTA-local level, kept for A/B
+    // runs: VX_QL_GLOBAL = intermediate in global memory (local.cuh),
+    // VX_QL_GROUP = padded shared-memory stage with lane-group networks
+    // (local2.cuh); both measured slower than local3.cuh
     static const bool global_local = getenv("VX_QL_GLOBAL") != nullptr;
     static const bool group_local = getenv("VX_QL_GROUP") != nullptr;
-    x.cluster_local = cluster_local;
-    x.global_local = global_local && !cluster_local;
-    x.group_local = group_local && !cluster_local && !global_local;
-    const bool q3 = !x.cluster_local && !x.global_local && !x.group_local;
+    x.global_local = global_local;
+    x.group_local = group_local && !global_local;
+    const bool q3 = !x.global_local && !x.group_local;
     const uint64_t ql_T = q3 ? Q3Cfg<K, V>::TARGET : (x.group_local ? Q2Cfg<K, V>::TARGET : QlCfg<K, V>::TARGET);
     uint64_t ql_Tmin = q3 ? Q3Cfg<K, V>::TMIN : (x.group_local ? Q2Cfg<K, V>::TMIN : QlCfg<K, V>::TMIN);
     // smallest n that takes the CTA-local level.  local3 is worth it as soon as
@@ -623,7 +616,6 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
         x.ql_target = (uint64_t)std::min((double)ql_T, std::max((double)ql_Tmin, ceil(t)));
     }
     x.ql_cap = !ql_on ? 0
-               : x.cluster_local ? QcCfg<K, V>::CAP
                : q3 ? Q3Cfg<K, V>::CAP
                : x.group_local ? Q2Cfg<K, V>::CAP
                                : QlCfg<K, V>::CAP;
@@ -638,33 +630,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     x.g_hist = x.sms * VX_OCC(qs_hist_kernel<K>, kQsNT, hist_smem_bytes<K>());
     x.g_scat = x.sms * VX_OCC((qs_scatter_kernel<K, V>), kQsNT, sizeof(ScatterPipeSmem<K, V>));
     x.g_fin = x.sms * VX_OCC((qs_finish_kernel<K, V>), kFinNT, sizeof(FinSmem<K, V>));
-    if (x.cluster_local) {
-        // persistent: as many 4-CTA clusters as fit at once
-        static int ncl_cache[kMaxDev] = {};
-        int& ncl = ncl_cache[cur_dev()];
-        if (!ncl) {
-            auto* kern = qs_localc_kernel<K, V>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QcSmem<K, V>));
-            cudaLaunchConfig_t lc = {};
-            lc.gridDim = dim3(kQcC * 64);
-            lc.blockDim = dim3(kQlNT);
-            lc.dynamicSmemBytes = sizeof(QcSmem<K, V>);
-            cudaLaunchAttribute at;
-            at.id = cudaLaunchAttributeClusterDimension;
-            at.val.clusterDim.x = kQcC;
-            at.val.clusterDim.y = 1;
-            at.val.clusterDim.z = 1;
-            lc.attrs = &at;
-            lc.numAttrs = 1;
-            int v = 0;
-            if (cudaOccupancyMaxActiveClusters(&v, (const void*)kern, &lc) != cudaSuccess || v <= 0) {
-                cudaGetLastError();
-                v = x.sms / kQcC;
-            }
-            ncl = v;
-        }
-        x.g_loc = ncl * kQcC;
-    } else if (x.global_local) {
+    if (x.global_local) {
         x.g_loc = x.sms * VX_OCC((qs_local_kernel<K, V>), kQlNT, sizeof(QlSmem<K, V>));
     } else if (x.group_local) {
         x.g_loc = x.sms * VX_OCC((qs_local2_kernel<K, V>), kQlNT, sizeof(Q2Smem<K, V>));

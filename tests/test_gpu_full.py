@@ -233,3 +233,34 @@ def test_pivot_strategies_same_output(tdt, n):
         vx.sort_into(x, out, vx.SortConfig(pivot_strategy=strategy, pivot_seed=7))
         outs.append(out)
     assert torch.equal(outs[0], torch.sort(x).values) and torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("env", ["VX_QL_GROUP", "VX_QL_GLOBAL", "VX_EAGER"])
+def test_opt_in_variants_still_sort(env):
+    """The A/B variants the library keeps behind environment switches (the
+    predecessors of the CTA-local level, the host-driven level loop) are read
+    once per process, so each runs in its own interpreter."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, paper_1704_08579_b200 as vx\n"
+        "from paper_1704_08579_b200.verify import generate, verify_sorted_permutation\n"
+        "for tdt, n in ((torch.int32, (1 << 24) + 5), (torch.float64, (1 << 23) + 3)):\n"
+        "    src = generate(tdt, 'uniform', n, seed=3)\n"
+        "    out = torch.empty_like(src)\n"
+        "    st = {}\n"
+        "    vx.sort_into(src, out, stats=st)\n"
+        "    verify_sorted_permutation(src, out)\n"
+        "    assert st['local_elems'] > n // 2, st\n"
+        "k = generate(torch.int32, 'uniform', 1 << 23, seed=4)\n"
+        "v = torch.arange(1 << 23, dtype=torch.int32, device='cuda')\n"
+        "k0 = k.clone()\n"
+        "vx.kv_sort(k, v)\n"
+        "assert bool((k[1:] >= k[:-1]).all()) and torch.equal(k0[v.long()], k)\n"
+        "print('ok')\n"
+    )
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, env: "1", "PYTHONPATH": root},
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
