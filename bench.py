@@ -540,10 +540,89 @@ def run_e2e(args, spec, vx, L, src, vals, dev, rank, world, units, extra):
             times.append(t1 - t0)
     total = allmax(sum(times))
     L.vx_host_release()
-    return {"value": units * args.steps / total / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(total / args.steps * 1e3, 3),
-            "path": "vx_host_* C ABI (host buffers)" if world == 1 and kind != "segments" else
-            "public API, pinned host tensors"}
+    res = {"value": units * args.steps / total / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h), "ms_per_step": round(total / args.steps * 1e3, 3),
+           "path": "vx_host_* C ABI (host buffers)" if world == 1 and kind != "segments" else
+           "public API, pinned host tensors"}
+    if world == 1 and kind in ("sort", "kv", "sharded") and not args.no_pipeline:
+        pipe = run_e2e_pipelined(args, vx, L, src, vals if kind == "kv" else None, host, hv, code, units)
+        if "value" in pipe:
+            # the headline e2e is the throughput of a stream of sorts through the
+            # pipelined boundary; the one-call-at-a-time figure stays beside it
+            res = {**pipe, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "single_call": {"value": res["value"], "ms_per_step": res["ms_per_step"], "path": res["path"]}}
+        else:
+            res["pipelined"] = pipe
+    return res
+
+
+def run_e2e_pipelined(args, vx, L, src, vals, host, hv, code, units):
+    """Throughput of a STREAM of host sorts: every step copies the pristine
+    pinned input in, sorts, and copies the result out to pinned memory, but
+    two steps are in flight (vx_host_sort_submit / vx_host_sort_wait), so one
+    step's copy-out overlaps the next step's copy-in over full-duplex PCIe."""
+    import torch
+
+    try:
+        outs = [torch.empty(src.shape, dtype=src.dtype, pin_memory=True) for _ in range(2)]
+        outv = [torch.empty(vals.shape, dtype=vals.dtype, pin_memory=True) for _ in range(2)] if vals is not None \
+            else [None, None]
+    except RuntimeError as e:  # not enough page-locked host memory on this box
+        return {"skipped": f"pinned output buffers: {e}"[:200]}
+    host.copy_(src)  # pristine input, read by every step, never written
+    if hv is not None:
+        hv.copy_(vals)
+    torch.cuda.synchronize()
+    lane = 16 if code == 0 else 8
+    n = host.numel()
+    vp = ctypes.c_void_p
+
+    def run(steps):
+        tickets = []
+        for i in range(steps):
+            if len(tickets) == 2:
+                rc = L.vx_host_sort_wait(tickets.pop(0))
+                assert rc == 0, L.vx_last_error()
+            t = ctypes.c_int(-1)
+            rc = L.vx_host_sort_submit(code, vp(host.data_ptr()), vp(hv.data_ptr()) if hv is not None else None,
+                                       vp(outs[i % 2].data_ptr()),
+                                       vp(outv[i % 2].data_ptr()) if hv is not None else None,
+                                       n, lane, 0, 0, 0, ctypes.byref(t))
+            assert rc == 0, L.vx_last_error()
+            tickets.append(t.value)
+        for t in tickets:
+            rc = L.vx_host_sort_wait(t)
+            assert rc == 0, L.vx_last_error()
+
+    run(max(2, args.warmup))  # both slots: arenas allocated, sort graphs built
+    barrier()
+    t0 = time.perf_counter()
+    run(args.steps)
+    total = allmax(time.perf_counter() - t0)
+    L.vx_host_release()
+    # gate: the last step's host output against the device sort of the same input
+    last = (args.steps - 1) % 2
+    want = torch.empty_like(src)
+    if vals is not None:
+        wantv = torch.empty_like(vals)
+        vx.sort_into(src, want, values=vals, out_values=wantv)
+        got = outs[last].to(src.device)
+        ok = bool(torch.equal(got, want))
+        gv = outv[last].to(src.device)
+        ok = ok and bool(torch.equal(src[gv.long()], got))  # values still name their keys
+        del wantv, gv
+    else:
+        vx.sort_into(src, want)
+        got = outs[last].to(src.device)
+        ok = bool(torch.equal(got, want))
+    del got, want
+    torch.cuda.empty_cache()
+    if not ok:
+        raise SystemExit("pipelined e2e output differs from the device sort")
+    return {"value": units * args.steps / total / 1e9, "unit": "Gelem/s",
+            "ms_per_step": round(total / args.steps * 1e3, 3), "verified": True,
+            "path": "vx_host_sort_submit / vx_host_sort_wait C ABI (pinned host buffers, 2 sorts in flight: "
+                    "copy-out of step i overlaps copy-in of step i+1)"}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -663,6 +742,7 @@ def main():
     ap.add_argument("--workload", default="c5_i32_uniform")
     ap.add_argument("--n", type=lambda s: int(eval(s, {}, {})), default=None, help="global n (e.g. 2**28)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="e2e: one synchronous host call per step only")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--prof-steps", type=int, default=2, help="steps of the per-kernel profiled pass")
     ap.add_argument("--exchange", default="collective", choices=["collective", "fused"],

@@ -223,7 +223,23 @@ int64_t vx_host_kv_scalar_partition(int dtype, void *keys, void *vals, int64_t l
 int vx_host_smallsort_region(int dtype, void *arr, int64_t lo, int64_t length);  /* _kernels.py:115 */
 int vx_host_kv_smallsort_region(int dtype, void *keys, void *vals, int64_t lo, int64_t length);
                                                                                  /* _kernels.py:148 */
-/* Free the device arena the host functions keep between calls. */
+/* Pipelined twins of vx_host_quicksort / vx_host_kv_quicksort for a STREAM of
+ * sorts (quicksort.py:115-134 called once per array).  A single in-place
+ * host sort is bound by PCIe one direction at a time (copy in, sort, copy
+ * out); vx_host_sort_submit enqueues copy-in, sort and copy-out of
+ * src -> dst (dst may equal src; vals NULL for keys only) on one of two
+ * device slots and returns at once, so the copy-out of one sort overlaps the
+ * copy-in of the next (full-duplex PCIe).  *ticket identifies the slot;
+ * vx_host_sort_wait(ticket) blocks until that sort's dst is complete and
+ * returns its status.  A third submit first waits for the oldest sort.
+ * Overlap needs page-locked host memory (vx_host_pin / cudaHostRegister, or
+ * a pinned allocator); pageable buffers are correct but serialise. */
+int vx_host_sort_submit(int dtype, const void *src_keys, const void *src_vals, void *dst_keys, void *dst_vals,
+                        int64_t n, int64_t lane, int64_t sort_bound, int strategy, uint64_t seed, int *ticket);
+int vx_host_sort_wait(int ticket);
+int vx_host_pin(void *p, size_t bytes);
+int vx_host_unpin(void *p);
+/* Free the device arenas the host functions keep between calls. */
 int vx_host_release(void);
 
 #ifdef __cplusplus

@@ -30,7 +30,7 @@ from .lanes import (
     native_available,
 )
 from .partition import partition_region, scalar_partition
-from .quicksort import SortConfig, select_pivot, sort, sort_into, sort_with_config
+from .quicksort import SortConfig, select_pivot, sort, sort_into, sort_many, sort_with_config
 from .sharded import sharded_sort
 from .smallsort import sort_segments, sort_small_region
 
@@ -40,6 +40,7 @@ __all__ = [
     "sort",
     "sort_with_config",
     "sort_into",
+    "sort_many",
     "SortConfig",
     "select_pivot",
     "partition_region",

@@ -94,6 +94,10 @@ def _declare(L):
         "vx_host_kv_scalar_partition": ([i32, vp, vp, i64, i64, vp], i64),
         "vx_host_smallsort_region": ([i32, vp, i64, i64], i32),
         "vx_host_kv_smallsort_region": ([i32, vp, vp, i64, i64], i32),
+        "vx_host_sort_submit": ([i32, vp, vp, vp, vp, i64, i64, i64, i32, u64, ctypes.POINTER(ctypes.c_int)], i32),
+        "vx_host_sort_wait": ([i32], i32),
+        "vx_host_pin": ([vp, sz], i32),
+        "vx_host_unpin": ([vp], i32),
         "vx_host_release": ([], i32),
     }
     for name, (args, res) in sigs.items():

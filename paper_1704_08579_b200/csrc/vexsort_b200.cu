@@ -827,6 +827,10 @@ struct HostArena {
     void* p = nullptr;
     size_t cap = 0;
     cudaStream_t st = nullptr;
+    // a submitted (pipelined) sort that has not been waited for yet
+    bool busy = false;
+    int last_rc = VX_OK;
+    Ctl* hstat = nullptr;  // pinned copy of the sort's status record
     int ensure(size_t bytes) {
         if (!st) VX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         if (bytes > cap) {
@@ -839,7 +843,12 @@ struct HostArena {
         return VX_OK;
     }
 };
-HostArena g_arenas[kMaxDev];  // one per device (the host API runs on the current device)
+// Per device (the host API runs on the current device): slot 0 serves the
+// synchronous calls and, with slot 1, the pipelined submit / wait pair.
+constexpr int kHostSlots = 2;
+HostArena g_slots[kMaxDev][kHostSlots];
+unsigned g_next_slot[kMaxDev];
+#define g_arenas(d) g_slots[d][0]
 
 int read_status(const void* ws, cudaStream_t st, vx_sort_stats* out) {
     unsigned long long* hp = g_pinned.get();
@@ -874,14 +883,27 @@ int check_lane(int dtype, int64_t lane) {
     return VX_OK;
 }
 
+// Finish the sort in flight on a slot: wait for its stream, turn the status
+// record it copied back into a return code.  Caller holds the slot's mutex.
+int host_slot_finish(HostArena& ar) {
+    if (!ar.busy) return ar.last_rc;
+    ar.busy = false;
+    if (cudaStreamSynchronize(ar.st) != cudaSuccess) return ar.last_rc = fail(VX_ECUDA, "pipelined sort: stream failed");
+    const Ctl* hc = ar.hstat;
+    if (hc->err & kErrLevels) return ar.last_rc = fail(VX_ECAPACITY, "sort exceeded the maximum level count");
+    if (hc->err) return ar.last_rc = fail(VX_ECAPACITY, "sort work-queue capacity exceeded");
+    return ar.last_rc = VX_OK;
+}
+
 int host_sort(int dtype, void* keys, void* vals, int64_t n, int64_t sort_bound, int strategy, int opt_a,
               int opt_b, uint64_t seed) {
     if (n < 2) return VX_OK;
     const size_t es = esize(dtype);
     const size_t data = align_up(n * es) * (vals ? 2 : 1);
     const size_t wsb = vx_sort_workspace_bytes(dtype, vals != nullptr, n);
-    HostArena& ar = g_arenas[cur_dev()];
+    HostArena& ar = g_arenas(cur_dev());
     std::lock_guard<std::mutex> lk(ar.mu);
+    host_slot_finish(ar);  // a pipelined sort still in flight on this slot
     int rc = ar.ensure(data + wsb);
     if (rc) return rc;
     char* d = static_cast<char*>(ar.p);
@@ -898,6 +920,56 @@ int host_sort(int dtype, void* keys, void* vals, int64_t n, int64_t sort_bound, 
     return read_status(d + data, st, nullptr);  // synchronises
 }
 
+// Pipelined host sort: enqueue copy-in, sort (as a CUDA graph: no host
+// synchronisation) and copy-out on the next slot's stream and return.  Two
+// slots, each with its own device arena and stream, so one sort's copy-out
+// (device -> host) overlaps the next sort's copy-in (host -> device): PCIe is
+// full duplex, and a single in-place sort can use only one direction at a
+// time.  The overlap needs page-locked host memory; pageable buffers work but
+// their copies serialise.
+int host_sort_submit(int dtype, const void* src_k, const void* src_v, void* dst_k, void* dst_v, int64_t n,
+                     int64_t sort_bound, int strategy, uint64_t seed, int* ticket) {
+    const int dev = cur_dev();
+    const int slot = (int)(g_next_slot[dev]++ % kHostSlots);
+    HostArena& ar = g_slots[dev][slot];
+    std::lock_guard<std::mutex> lk(ar.mu);
+    host_slot_finish(ar);  // a sort nobody waited for: its buffers are about to be reused
+    if (ticket) *ticket = slot;
+    ar.last_rc = VX_OK;
+    const size_t es = esize(dtype);
+    if (n < 2) {
+        if (n == 1 && dst_k != src_k) {
+            std::memcpy(dst_k, src_k, es);
+            if (src_v) std::memcpy(dst_v, src_v, es);
+        }
+        return VX_OK;
+    }
+    const size_t data = align_up(n * es) * (src_v ? 2 : 1);
+    const size_t wsb = vx_sort_workspace_bytes(dtype, src_v != nullptr, n);
+    if (int rc = ar.ensure(data + wsb)) return rc;
+    if (!ar.hstat) VX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ar.hstat), sizeof(Ctl), cudaHostAllocDefault));
+    char* d = static_cast<char*>(ar.p);
+    void* dk = d;
+    void* dv = src_v ? d + align_up(n * es) : nullptr;
+    cudaStream_t st = ar.st;
+    VX_CUDA(cudaMemcpyAsync(dk, src_k, n * es, cudaMemcpyHostToDevice, st));
+    if (src_v) VX_CUDA(cudaMemcpyAsync(dv, src_v, n * es, cudaMemcpyHostToDevice, st));
+    vx_sort_config cfg{sort_bound, strategy, 0, 0, VX_SORT_GRAPH, seed};
+    if (int rc = vx_sort(dtype, dk, dv, n, &cfg, d + data, wsb, (vx_stream_t)st)) return ar.last_rc = rc;
+    VX_CUDA(cudaMemcpyAsync(dst_k, dk, n * es, cudaMemcpyDeviceToHost, st));
+    if (src_v) VX_CUDA(cudaMemcpyAsync(dst_v, dv, n * es, cudaMemcpyDeviceToHost, st));
+    VX_CUDA(cudaMemcpyAsync(ar.hstat, d + data + 2 * sizeof(Ctl), sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    ar.busy = true;
+    return VX_OK;
+}
+
+int host_sort_wait(int ticket) {
+    if (ticket < 0 || ticket >= kHostSlots) return fail(VX_EINVAL, "unknown ticket");
+    HostArena& ar = g_slots[cur_dev()][ticket];
+    std::lock_guard<std::mutex> lk(ar.mu);
+    return host_slot_finish(ar);
+}
+
 int64_t host_partition(int dtype, void* keys, void* vals, int64_t lo, int64_t hi, const void* pivot) {
     if (hi < lo || lo < 0) return fail(VX_EINVAL, "bad range");
     const int64_t n = hi - lo;
@@ -908,8 +980,9 @@ int64_t host_partition(int dtype, void* keys, void* vals, int64_t lo, int64_t hi
     const size_t a = align_up(n * es);
     const size_t nbuf = vals ? 4 : 2;
     const size_t wsb = vx_partition_workspace_bytes(dtype, n);
-    HostArena& ar = g_arenas[cur_dev()];
+    HostArena& ar = g_arenas(cur_dev());
     std::lock_guard<std::mutex> lk(ar.mu);
+    host_slot_finish(ar);
     int rc = ar.ensure(nbuf * a + 256 + wsb);
     if (rc) return rc;
     char* d = static_cast<char*>(ar.p);
@@ -1317,12 +1390,37 @@ int vx_host_kv_smallsort_region(int dtype, void* keys, void* vals, int64_t lo, i
                      0, 0);
 }
 
+int vx_host_sort_submit(int dtype, const void* src_keys, const void* src_vals, void* dst_keys, void* dst_vals,
+                        int64_t n, int64_t lane, int64_t sort_bound, int strategy, uint64_t seed, int* ticket) {
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_lane(dtype, lane)) return rc;
+    if (strategy < 0 || strategy > 2) return fail(VX_EINVAL, "unknown pivot strategy");
+    if (n < 0 || (n > 0 && (!src_keys || !dst_keys))) return fail(VX_EINVAL, "null keys");
+    if ((src_vals == nullptr) != (dst_vals == nullptr)) return fail(VX_EINVAL, "values: give both or neither");
+    return host_sort_submit(dtype, src_keys, src_vals, dst_keys, dst_vals, n, sort_bound, strategy, seed, ticket);
+}
+
+int vx_host_sort_wait(int ticket) { return host_sort_wait(ticket); }
+
+int vx_host_pin(void* p, size_t bytes) {
+    VX_CUDA(cudaHostRegister(p, bytes, cudaHostRegisterDefault));
+    return VX_OK;
+}
+
+int vx_host_unpin(void* p) {
+    VX_CUDA(cudaHostUnregister(p));
+    return VX_OK;
+}
+
 int vx_host_release(void) {
-    HostArena& ar = g_arenas[cur_dev()];
-    std::lock_guard<std::mutex> lk(ar.mu);
-    if (ar.p) VX_CUDA(cudaFree(ar.p));
-    ar.p = nullptr;
-    ar.cap = 0;
+    for (int s = 0; s < kHostSlots; ++s) {
+        HostArena& ar = g_slots[cur_dev()][s];
+        std::lock_guard<std::mutex> lk(ar.mu);
+        host_slot_finish(ar);
+        if (ar.p) VX_CUDA(cudaFree(ar.p));
+        ar.p = nullptr;
+        ar.cap = 0;
+    }
     return VX_OK;
 }
 

@@ -143,6 +143,39 @@ def sort_into(src, out, config: SortConfig | None = None, values=None, out_value
     return _device_sort(kind, src, values, out, out_values, config, bound, check, "sort_into", stats)
 
 
+def sort_many(regions, config: SortConfig | None = None, out=None) -> None:
+    """Sort a sequence of HOST regions (numpy arrays / CPU tensors), each
+    ascending in place -- ``for r in regions: sort(r, config)`` with the
+    copies pipelined: while one region's sorted keys travel back over PCIe
+    the next region's input is already on its way in (two device slots,
+    ``vx_host_sort_submit`` / ``vx_host_sort_wait``).  ``out`` (optional, same
+    shapes) receives the sorted copies and leaves ``regions`` untouched.
+    Page-locked regions (``tensor.pin_memory()``) are needed for the overlap;
+    pageable ones give the same result at ``sort``'s speed."""
+    config = config or SortConfig()
+    regions = list(regions)
+    outs = regions if out is None else list(out)
+    assert len(outs) == len(regions), "out must match regions"
+    L = lib()
+    pending: list[int] = []
+    for src, dst in zip(regions, outs):
+        kind = check_region(src)
+        assert not is_device(src) and not is_device(dst), "sort_many takes host regions; use sort() for CUDA tensors"
+        if dst is not src:
+            assert check_region(dst) is kind and len(dst) == len(src), "out region must match its source"
+        backend = get_backend(config.backend, kind)
+        bound = _resolve_bound(config, backend.lanes)
+        if len(pending) == 2:
+            check(L.vx_host_sort_wait(pending.pop(0)), "sort_many")
+        t = ctypes.c_int(-1)
+        check(L.vx_host_sort_submit(kind.code, host_ptr(src), None, host_ptr(dst), None, len(src), backend.lanes,
+                                    bound, _PIVOT_STRATEGIES.index(config.pivot_strategy),
+                                    int(config.pivot_seed) & _U64, ctypes.byref(t)), "sort_many")
+        pending.append(t.value)
+    for t in pending:
+        check(L.vx_host_sort_wait(t), "sort_many")
+
+
 def sort(region, config: SortConfig | None = None) -> None:
     """Sort a region of int32 or float64 ascending, in place (quicksort.py:137-143).
     NaN elements are unsupported."""

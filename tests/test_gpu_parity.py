@@ -654,3 +654,70 @@ def test_c5_f64_distributions_2_24(dist):
     ref = torch.sort(t)[0]  # independent comparator (library sort, test only)
     out = vx.sharded_sort(t)  # P = 1 path (out of place)
     assert torch.equal(out, ref)
+
+
+# ------------------------------------------------- pipelined host sorts
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_sort_many_pipelined_host_regions(dt):
+    """sort_many == sort on every region (quicksort.py:137-143 per array),
+    with pinned, pageable, empty and single-element regions in one stream."""
+    rng = np.random.default_rng(11)
+    sizes = [0, 1, 2, 257, 5000, 1 << 16, (1 << 20) + 3, 1 << 21, 77, 1 << 18]
+    arrs = []
+    for i, n in enumerate(sizes):
+        a = (rng.integers(-(2**31), 2**31 - 1, size=n, endpoint=True).astype(np.int32) if dt is np.int32
+             else rng.standard_normal(n) * 1e3)
+        arrs.append(a)
+    want = []
+    for a in arrs:
+        w = a.copy()
+        oracle.sort(w)
+        want.append(w)
+    regs = [torch.from_numpy(a.copy()).pin_memory() if i % 2 == 0 else a.copy() for i, a in enumerate(arrs)]
+    vx.sort_many(regs)
+    for r, w in zip(regs, want):
+        got = r.numpy() if isinstance(r, torch.Tensor) else r
+        assert np.array_equal(got, w)
+    # out-of-place: sources untouched, sorted copies in `out`
+    srcs = [torch.from_numpy(a.copy()).pin_memory() for a in arrs]
+    outs = [torch.empty_like(s).pin_memory() for s in srcs]
+    vx.sort_many(srcs, out=outs)
+    for s, a, o, w in zip(srcs, arrs, outs, want):
+        assert np.array_equal(s.numpy(), a) and np.array_equal(o.numpy(), w)
+
+
+def test_host_submit_wait_contract():
+    """Tickets name one of two slots; a third submit waits for the oldest
+    sort; the synchronous host calls may be mixed in; bad arguments fail the
+    way the synchronous twins do."""
+    import ctypes
+
+    from paper_1704_08579_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    bufs = [torch.from_numpy(rng.integers(-1000, 1000, size=300000).astype(np.int32)).pin_memory() for _ in range(5)]
+    want = [np.sort(b.numpy()) for b in bufs]
+    tickets = []
+    for b in bufs:
+        t = ctypes.c_int(-1)
+        p = ctypes.c_void_p(b.data_ptr())
+        assert L.vx_host_sort_submit(0, p, None, p, None, b.numel(), 16, 0, 0, 0, ctypes.byref(t)) == 0
+        assert t.value in (0, 1)
+        tickets.append(t.value)
+    x = rng.integers(-5, 5, size=1000).astype(np.int32)
+    vx.sort(x)  # synchronous call while two submits are in flight
+    assert np.array_equal(x, np.sort(x))
+    assert L.vx_host_sort_wait(0) == 0 and L.vx_host_sort_wait(1) == 0
+    assert L.vx_host_sort_wait(0) == 0  # idempotent
+    for b, w in zip(bufs, want):
+        assert np.array_equal(b.numpy(), w)
+    assert L.vx_host_sort_wait(7) == -1
+    t = ctypes.c_int(-1)
+    p = ctypes.c_void_p(bufs[0].data_ptr())
+    assert L.vx_host_sort_submit(0, p, None, p, None, 10, 8, 0, 0, 0, ctypes.byref(t)) == -1  # lane / kind mismatch
+    assert L.vx_host_sort_submit(5, p, None, p, None, 10, 16, 0, 0, 0, ctypes.byref(t)) == -2  # dtype
+    assert L.vx_host_sort_submit(0, p, p, p, None, 10, 16, 0, 0, 0, ctypes.byref(t)) == -1  # values: both or neither
+    L.vx_host_release()
