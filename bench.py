@@ -151,13 +151,20 @@ def dist_setup(n_gpus):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus and world > 1:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    # VX_BENCH_SHARE_GPU=1 (with VX_BENCH_BACKEND=gloo): every rank on cuda:0 with
+    # host-staged collectives -- a functional check of the N > 1 code path on a
+    # one-GPU box (tests/test_gpu_sharded.py), never a measurement
+    if os.environ.get("VX_BENCH_SHARE_GPU"):
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import datetime
 
+        backend = os.environ.get("VX_BENCH_BACKEND", "nccl")
+        kw = {"device_id": torch.device("cuda", local)} if backend == "nccl" else {}
         # a hung peer fails the run within minutes instead of blocking forever
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local),
-                                timeout=datetime.timedelta(seconds=int(os.environ.get("VX_PG_TIMEOUT", "600"))))
+        dist.init_process_group(backend, timeout=datetime.timedelta(seconds=int(os.environ.get("VX_PG_TIMEOUT", "600"))),
+                                **kw)
     return rank, world, local
 
 
@@ -740,7 +747,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c5_i32_uniform")
-    ap.add_argument("--n", type=lambda s: int(eval(s, {}, {})), default=None, help="global n (e.g. 2**28)")
+    ap.add_argument("--n", "--size", dest="n", type=lambda s: int(eval(s, {}, {})), default=None, help="global n (e.g. 2**28)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="e2e: one synchronous host call per step only")
     ap.add_argument("--no-cpu", action="store_true")
