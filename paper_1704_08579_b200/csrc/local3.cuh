@@ -51,6 +51,16 @@ namespace vx {
 #ifndef VX_Q3_LT10
 #define VX_Q3_LT10 97  // largest mean bucket x 10 for 16-slot lanes
 #endif
+#ifndef VX_Q3_NT
+#define VX_Q3_NT kQlNT  // threads per CTA
+#endif
+#ifndef VX_Q3_CTAS
+#define VX_Q3_CTAS 1  // resident CTAs per SM (the stage and table must fit that many times)
+#endif
+#ifndef VX_Q3_NB
+#define VX_Q3_NB 12288  // bucket table capacity
+#endif
+constexpr unsigned kQ3NT = VX_Q3_NT;
 
 template <typename K, typename V>
 struct Q3Cfg {
@@ -58,9 +68,9 @@ struct Q3Cfg {
     static constexpr unsigned BYTES = sizeof(K) + (KV ? sizeof(V) : 0);
     static constexpr int LE = BYTES <= 8 ? 16 : 8;  // slots a lane sorts in registers
     static constexpr unsigned LT10 = LE == 16 ? VX_Q3_LT10 : VX_Q3_LT10 / 2;
-    static constexpr unsigned ROUND = kQlNT;  // buckets per round: one per lane
-    static constexpr unsigned NB = 12288;     // bucket table capacity (leaves up to ~2.8x the 4-byte target)
-    static constexpr unsigned BPT = NB / kQlNT;
+    static constexpr unsigned ROUND = kQ3NT;  // buckets per round: one per lane
+    static constexpr unsigned NB = VX_Q3_NB;  // bucket table capacity (leaves up to ~2.8x the 4-byte target)
+    static constexpr unsigned BPT = NB / kQ3NT;
     static constexpr unsigned TAIL = 256 + 16;  // sentinel slots after the image (the widest network + alignment)
     static constexpr unsigned SLOTS = VX_Q3_STAGE_BYTES / BYTES;
     static constexpr unsigned SCAP = SLOTS - TAIL - 16;  // largest image
@@ -86,8 +96,8 @@ struct Q3Smem {
     unsigned tab[C::NB];             // bucket counts; then image cursor << 16 | count
     unsigned gstart[C::MAXG + 1];    // offset in the sorted leaf where group g starts
     unsigned gfirst[C::MAXG + 1];    // first bucket of group g
-    typename OKey<K>::U rmin[kQlNT / 32], rmax[kQlNT / 32];
-    unsigned scan[kQlNT / 32 + 1];
+    typename OKey<K>::U rmin[kQ3NT / 32], rmax[kQ3NT / 32];
+    unsigned scan[kQ3NT / 32 + 1];
 };
 
 // One lane sorts the E consecutive image slots that start at its bucket and
@@ -232,7 +242,7 @@ __device__ __forceinline__ void image_store_async(const T* img, T* __restrict__ 
 }
 
 template <typename K, typename V>
-__global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
+__global__ void __launch_bounds__(kQ3NT, VX_Q3_CTAS) qs_local3_kernel(const QlItem* __restrict__ items, Ctl* __restrict__ ctl,
                                                              Ctl* __restrict__ ctl_next, Seg* __restrict__ next_segs,
                                                              unsigned cap_seg, const K* __restrict__ src_k,
                                                              const V* __restrict__ src_v, K* __restrict__ oth_k,
@@ -241,7 +251,7 @@ __global__ void __launch_bounds__(kQlNT, 1) qs_local3_kernel(const QlItem* __res
     using C = Q3Cfg<K, V>;
     using U = typename OKey<K>::U;
     constexpr bool KV = HasVal<V>::value;
-    constexpr unsigned NT = kQlNT, BPT = C::BPT;
+    constexpr unsigned NT = kQ3NT, BPT = C::BPT;
     constexpr int LE = C::LE;
     constexpr unsigned VE = 16 / sizeof(K);
     extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -286,7 +286,7 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
                 x.keys, x.vals, x.leaf);
         else if (!x.global_local)  // default: sorted image in shared memory, one lane per bucket (local3.cuh)
-            qs_local3_kernel<K, V><<<x.g_loc, kQlNT, sizeof(Q3Smem<K, V>), st>>>(
+            qs_local3_kernel<K, V><<<x.g_loc, kQ3NT, sizeof(Q3Smem<K, V>), st>>>(
                 x.qls, c, nx, x.segs[p ^ 1], x.cap_seg, dst_k, dst_v, p ? x.sk : x.keys, p ? x.sv : x.vals,
                 x.keys, x.vals, x.leaf);
         else  // opt-in: intermediate through L2 in the other buffer
@@ -652,7 +652,7 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     } else if (x.group_local) {
         x.g_loc = x.sms * VX_OCC((qs_local2_kernel<K, V>), kQlNT, sizeof(Q2Smem<K, V>));
     } else {
-        x.g_loc = x.sms * VX_OCC((qs_local3_kernel<K, V>), kQlNT, sizeof(Q3Smem<K, V>));
+        x.g_loc = x.sms * VX_OCC((qs_local3_kernel<K, V>), kQ3NT, sizeof(Q3Smem<K, V>));
     }
     x.g_seg = 2 * x.sms;
 
