@@ -25,7 +25,10 @@ roofline = the dominant kernel class: algorithmic bytes (one read + one
          write of every element it processed) / its summed
          CUDA-event time, against MEASURED_PEAKS.json hbm_gbs.
 cpu_baseline = the CPU oracle (C port of the reference's _kernels.py,
-         OpenMP task-parallel variant, identical output) on a bounded sample.
+         OpenMP task-parallel variant, identical output) on a bounded sample,
+         the same port on one thread, and -- when the copy of the reference
+         package in baseline/_ref travels with the repo -- the reference's own
+         numba backend on one pinned core.
 --impl reference: only that CPU port, rank 0, same metric and unit.
 """
 
@@ -716,7 +719,78 @@ def cpu_baseline(spec, args, src=None):
         # BASELINE.md section 3 quotes the reference on ONE core: the same port, one thread
         n1, sec1 = cpu_run_once(spec, sample, 1)
         out["single_core"] = {"value": n1 / sec1 / 1e9, "unit": "Gelem/s", "cores": 1, "seconds": round(sec1, 2)}
+    ref = numba_reference(spec, sample)
+    if ref is not None:
+        out["reference_numba"] = ref
     return out
+
+
+def numba_reference(spec, sample):
+    """BASELINE.md section 3's setting, when a copy of the reference package
+    travels with the repo (baseline/_ref, made by tests/golden/make_golden.py):
+    the reference's own numba backend through its public API, ONE pinned
+    core, JIT call excluded, on a (smaller) prefix of the same sample.
+    Returns None when the copy or numba is missing."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "vexsort")):
+        return None
+    try:
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import numpy as np
+        import vexsort
+
+        if not vexsort.native_available():
+            return None
+    except Exception:  # noqa: BLE001  (numba missing / import error: no reference figure)
+        return None
+    kind = spec["kind"]
+    old_aff = os.sched_getaffinity(0)
+    core = min(old_aff)
+    try:
+        os.sched_setaffinity(0, {core})
+        if kind in ("sort", "sharded"):
+            a = sample[: 1 << 22].copy()
+            vexsort.sort(a[: 1 << 12].copy())  # JIT
+            t0 = time.perf_counter()
+            vexsort.sort(a)
+            sec, n, what = time.perf_counter() - t0, len(a), "vexsort.sort"
+            ok = bool(np.all(a[1:] >= a[:-1]))
+        elif kind == "kv":
+            k, v = sample[0][: 1 << 21].copy(), sample[1][: 1 << 21].copy()
+            vexsort.kv_sort(k[: 1 << 12].copy(), v[: 1 << 12].copy())
+            t0 = time.perf_counter()
+            vexsort.kv_sort(k, v)
+            sec, n, what = time.perf_counter() - t0, len(k), "vexsort.kv_sort"
+            ok = bool(np.all(k[1:] >= k[:-1]))
+        elif kind == "partition":
+            a = sample[: 1 << 24].copy()
+            piv = float(a[vexsort.select_pivot(a, 0, len(a) - 1)])
+            vexsort.partition_region(a[: 1 << 12].copy(), piv)
+            t0 = time.perf_counter()
+            b = vexsort.partition_region(a, piv)
+            sec, n, what = time.perf_counter() - t0, len(a), "vexsort.partition_region"
+            ok = bool(np.all(a[:b] <= piv) and np.all(a[b:] > piv))
+        else:  # segments: one small sort per segment, as BASELINE.md section 2 timed it
+            from vexsort import _kernels
+
+            offs, vals = sample
+            nseg = min(len(offs) - 1, 1 << 13)
+            a = vals[: int(offs[nseg])].copy()
+            sent = np.iinfo(np.int32).max if a.dtype == np.int32 else np.inf
+            _kernels.smallsort_region(a[:64].copy(), 0, 64, sent)
+            t0 = time.perf_counter()
+            for i in range(nseg):
+                _kernels.smallsort_region(a, int(offs[i]), int(offs[i + 1] - offs[i]), sent)
+            sec, n, what = time.perf_counter() - t0, len(a), f"_kernels.smallsort_region x {nseg} segments"
+            ok = True
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": repr(e)[:160]}
+    finally:
+        os.sched_setaffinity(0, old_aff)
+    return {"value": n / sec / 1e9, "unit": "Gelem/s", "cores": 1, "kind": "reference",
+            "sample": f"{what} (numba backend, baseline/_ref copy of the reference), first {n} elements of the "
+                      f"sample, pinned to core {core}, {sec:.2f} s, output ordered: {ok}"}
 
 
 def run_reference(args, spec, rank):
@@ -734,9 +808,13 @@ def run_reference(args, spec, rank):
         tot_n += n
         tot_s += s
     v = tot_n / tot_s / 1e9
+    cb = {"value": v, "unit": "Gelem/s", "cores": nt, "kind": "port",
+          "sample": f"{desc} per step; C port of _kernels.py (oracle/)"}
+    ref = numba_reference(spec, sample)
+    if ref is not None:
+        cb["reference_numba"] = ref
     return {"value": v, "ms": tot_s / args.steps * 1e3,
-            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": nt, "kind": "port",
-                             "sample": f"{desc} per step; C port of _kernels.py (oracle/)"},
+            "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

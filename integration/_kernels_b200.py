@@ -53,6 +53,8 @@ def _lib():
         L.vx_host_kv_partition.restype = i64
         L.vx_host_smallsort_region.argtypes = [i32, vp, i64, i64]
         L.vx_host_kv_smallsort_region.argtypes = [i32, vp, vp, i64, i64]
+        L.vx_host_sort_submit.argtypes = [i32, vp, vp, vp, vp, i64, i64, i64, i32, u64, ctypes.POINTER(ctypes.c_int)]
+        L.vx_host_sort_wait.argtypes = [i32]
         L.vx_last_error.restype = ctypes.c_char_p
         L.vx_version.restype = i32
         _L = L
@@ -153,6 +155,24 @@ def smallsort_region(arr, lo, length, sentinel):  # _kernels.py:115
 def kv_smallsort_region(keys, vals, lo, length, sentinel):  # _kernels.py:148
     _count("kv_smallsort_region")
     _ok(_lib().vx_host_kv_smallsort_region(_dt(keys), _ptr(keys), _ptr(vals), int(lo), int(length)))
+
+
+def quicksort_many(arrays, lane, sort_bound, sentinel, strategy, opt_a, opt_b, seed):
+    """``for a in arrays: quicksort(a, ...)`` (quicksort.py:124-133 once per
+    array) with the PCIe copies of consecutive arrays overlapped: two sorts
+    in flight through vx_host_sort_submit / vx_host_sort_wait."""
+    _count("quicksort_many")
+    L = _lib()
+    pending = []
+    for a in arrays:
+        if len(pending) == 2:
+            _ok(L.vx_host_sort_wait(pending.pop(0)))
+        t = ctypes.c_int(-1)
+        _ok(L.vx_host_sort_submit(_dt(a), _ptr(a), None, _ptr(a), None, len(a), lane, sort_bound, strategy,
+                                  seed & (2**64 - 1), ctypes.byref(t)))
+        pending.append(t.value)
+    for t in pending:
+        _ok(L.vx_host_sort_wait(t))
 
 
 def install() -> None:

@@ -162,6 +162,26 @@ __device__ __forceinline__ unsigned warp_rank_add(unsigned* cnt, unsigned b) {
     return atomicAdd(&cnt[b], 1u);
 }
 
+// src[0, n) -> dst[0, n) by the whole CTA of NT threads: 16-byte vectors over
+// the body when both share a 16-byte phase (true for the same offset into two
+// equally aligned buffers), element copies otherwise.
+template <typename T, unsigned NT>
+__device__ __forceinline__ void cta_copy(const T* __restrict__ src, T* __restrict__ dst, unsigned n) {
+    constexpr unsigned VE = 16 / sizeof(T);
+    if (((reinterpret_cast<uintptr_t>(src) ^ reinterpret_cast<uintptr_t>(dst)) & 15) != 0) {
+        for (unsigned i = threadIdx.x; i < n; i += NT) dst[i] = src[i];
+        return;
+    }
+    const unsigned head = min(n, (unsigned)(((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) / sizeof(T)));
+    const unsigned nv = (n - head) / VE;
+    if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (unsigned j = threadIdx.x; j < nv; j += NT) d4[j] = __ldcs(s4 + j);
+    const unsigned t0 = head + nv * VE;
+    if (t0 + threadIdx.x < n) dst[t0 + threadIdx.x] = src[t0 + threadIdx.x];
+}
+
 // 64-bit hash (splitmix64 finaliser) for deterministic sample positions.
 __host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     x += 0x9E3779B97F4A7C15ULL;

@@ -522,10 +522,8 @@ __global__ void __launch_bounds__(kFinNT, 2) qs_finish_kernel(const Fin* __restr
         const K* sk = (f.flags & 1u) ? scr_k : data_k;
         const V* sv = (f.flags & 1u) ? scr_v : data_v;
         if (f.flags & 2u) {
-            for (unsigned i = threadIdx.x; i < f.len; i += kFinNT) {
-                data_k[f.start + i] = sk[f.start + i];
-                if constexpr (KV) data_v[f.start + i] = sv[f.start + i];
-            }
+            cta_copy<K, kFinNT>(sk + f.start, data_k + f.start, f.len);
+            if constexpr (KV) cta_copy<V, kFinNT>(sv + f.start, data_v + f.start, f.len);
         } else if (f.len <= min(wmax, 256u)) {
             if (threadIdx.x < 32) warp_sort_any2<K, V>(sk + f.start, sv ? sv + f.start : nullptr, data_k + f.start,
                                                        data_v ? data_v + f.start : nullptr, f.len);

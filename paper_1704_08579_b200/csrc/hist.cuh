@@ -26,8 +26,11 @@ namespace vx {
 #ifndef VX_HIST_STAGES4
 #define VX_HIST_STAGES4 4
 #endif
+#ifndef VX_HIST_STAGES8
+#define VX_HIST_STAGES8 2
+#endif
 template <typename K>
-constexpr int hist_stages() { return sizeof(K) == 4 ? VX_HIST_STAGES4 : 2; }
+constexpr int hist_stages() { return sizeof(K) == 4 ? VX_HIST_STAGES4 : VX_HIST_STAGES8; }
 
 template <typename K>
 constexpr unsigned hist_stage_bytes() {

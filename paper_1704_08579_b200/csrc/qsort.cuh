@@ -845,15 +845,18 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                 const bool final_ = c == 1 || (sg.mode == 1 ? (sg.mul == 0) : sg.mode == 0 && (b & 1u) != 0);
                 if (final_) {
                     if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
-                        const unsigned nch = (unsigned)((c + kCopyChunk - 1) / kCopyChunk);
+                        // (this thread writes every chunk record: at most ~1024 per bucket)
+                        const unsigned long long chunk =
+                            max((unsigned long long)kCopyChunk, ((c >> 10) + 4095ull) & ~4095ull);
+                        const unsigned nch = (unsigned)((c + chunk - 1) / chunk);
                         unsigned f = atomicAdd(&ctl->fin_ctr, nch);
                         if (f + nch > cap_fin) {
                             atomicOr(&ctl->err, kErrCapacity);
                         } else {
                             for (unsigned i = 0; i < nch; ++i) {
-                                const unsigned long long o = (unsigned long long)i * kCopyChunk;
+                                const unsigned long long o = (unsigned long long)i * chunk;
                                 fins[f + i].start = bstart + o;
-                                fins[f + i].len = (unsigned)min((unsigned long long)kCopyChunk, c - o);
+                                fins[f + i].len = (unsigned)min(chunk, c - o);
                                 fins[f + i].flags = 3u;
                             }
                         }

@@ -4,6 +4,7 @@
 // qsort.cuh) are instantiated here for the element kinds of the reference
 // (int32, float64) and their same-width payloads (uint32 / uint64).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -864,7 +865,7 @@ struct HostArena {
 // synchronous calls and, with slot 1, the pipelined submit / wait pair.
 constexpr int kHostSlots = 2;
 HostArena g_slots[kMaxDev][kHostSlots];
-unsigned g_next_slot[kMaxDev];
+std::atomic<unsigned> g_next_slot[kMaxDev];
 #define g_arenas(d) g_slots[d][0]
 
 int read_status(const void* ws, cudaStream_t st, vx_sort_stats* out) {
@@ -947,7 +948,7 @@ int host_sort(int dtype, void* keys, void* vals, int64_t n, int64_t sort_bound, 
 int host_sort_submit(int dtype, const void* src_k, const void* src_v, void* dst_k, void* dst_v, int64_t n,
                      int64_t sort_bound, int strategy, uint64_t seed, int* ticket) {
     const int dev = cur_dev();
-    const int slot = (int)(g_next_slot[dev]++ % kHostSlots);
+    const int slot = (int)(g_next_slot[dev].fetch_add(1) % kHostSlots);
     HostArena& ar = g_slots[dev][slot];
     std::lock_guard<std::mutex> lk(ar.mu);
     host_slot_finish(ar);  // a sort nobody waited for: its buffers are about to be reused

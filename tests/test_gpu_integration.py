@@ -96,3 +96,22 @@ def test_reference_kv_api_through_b200_kernels():
     r = subprocess.run([sys.executable, "-c", code], cwd=REF, env=_env(), capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, (r.stdout + r.stderr)[-3000:]
+
+
+def test_stub_quicksort_many_pipelined():
+    """The stub's pipelined loop (vx_host_sort_submit / vx_host_sort_wait)
+    gives what one `_kernels.quicksort` call per array gives."""
+    import numpy as np
+
+    sys.path.insert(0, ROOT)
+    import integration._kernels_b200 as kb
+
+    rng = np.random.default_rng(2)
+    arrays = [rng.integers(-(2**31), 2**31 - 1, size=n, dtype=np.int32) for n in (5, 70000, 1 << 20, 0, 333, 1 << 19)]
+    arrays += [rng.standard_normal(n) for n in (1, 4097, 1 << 18)]
+    want = [np.sort(a) for a in arrays]
+    kb.quicksort_many([a for a in arrays if a.dtype == np.int32], 16, 256, 2**31 - 1, 0, False, False, 0)
+    kb.quicksort_many([a for a in arrays if a.dtype == np.float64], 8, 128, np.inf, 0, False, False, 0)
+    for a, w in zip(arrays, want):
+        assert np.array_equal(a, w)
+    assert kb.CALLS.get("quicksort_many") == 2

@@ -721,3 +721,34 @@ def test_host_submit_wait_contract():
     assert L.vx_host_sort_submit(5, p, None, p, None, 10, 16, 0, 0, 0, ctypes.byref(t)) == -2  # dtype
     assert L.vx_host_sort_submit(0, p, p, p, None, 10, 16, 0, 0, 0, ctypes.byref(t)) == -1  # values: both or neither
     L.vx_host_release()
+
+
+def test_host_submit_wait_pairs_out_of_place():
+    """Pipelined key/value sorts (vx_host_sort_submit with values): keys
+    bit-exact, values still name their keys, sources untouched."""
+    import ctypes
+
+    from paper_1704_08579_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(9)
+    vp = ctypes.c_void_p
+    jobs = []
+    for n, kdt, vdt, lane in ((200000, np.int32, np.int32, 16), (1 << 20, np.float64, np.int64, 8),
+                              (4099, np.int32, np.int32, 16)):
+        k = (rng.integers(0, 2**31, size=n).astype(kdt) if kdt is np.int32 else rng.standard_normal(n))
+        v = np.arange(n, dtype=vdt)
+        sk, sv = torch.from_numpy(k.copy()).pin_memory(), torch.from_numpy(v.copy()).pin_memory()
+        dk, dv = torch.empty_like(sk).pin_memory(), torch.empty_like(sv).pin_memory()
+        t = ctypes.c_int(-1)
+        rc = L.vx_host_sort_submit(0 if kdt is np.int32 else 1, vp(sk.data_ptr()), vp(sv.data_ptr()),
+                                   vp(dk.data_ptr()), vp(dv.data_ptr()), n, lane, 0, 0, 0, ctypes.byref(t))
+        assert rc == 0, L.vx_last_error()
+        jobs.append((k, v, sk, sv, dk, dv, t.value))
+    for k, v, sk, sv, dk, dv, t in jobs:
+        assert L.vx_host_sort_wait(t) == 0
+        assert np.array_equal(sk.numpy(), k) and np.array_equal(sv.numpy(), v)
+        assert np.array_equal(dk.numpy(), np.sort(k))
+        assert np.array_equal(k[dv.numpy()], dk.numpy())
+        assert np.array_equal(np.sort(dv.numpy()), v)
+    L.vx_host_release()
