@@ -177,7 +177,18 @@ __device__ __forceinline__ void cta_copy(const T* __restrict__ src, T* __restric
     if (threadIdx.x < head) dst[threadIdx.x] = src[threadIdx.x];
     const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
     uint4* d4 = reinterpret_cast<uint4*>(dst + head);
-    for (unsigned j = threadIdx.x; j < nv; j += NT) d4[j] = __ldcs(s4 + j);
+    // four loads in flight per thread before the first store (a 512-thread CTA
+    // then keeps 32 KB on the way, enough to cover HBM latency at two CTAs per SM)
+    unsigned j = threadIdx.x;
+    for (; j + 3 * NT < nv; j += 4 * NT) {
+        const uint4 a = __ldcs(s4 + j), b = __ldcs(s4 + j + NT), c = __ldcs(s4 + j + 2 * NT),
+                    e = __ldcs(s4 + j + 3 * NT);
+        d4[j] = a;
+        d4[j + NT] = b;
+        d4[j + 2 * NT] = c;
+        d4[j + 3 * NT] = e;
+    }
+    for (; j < nv; j += NT) d4[j] = __ldcs(s4 + j);
     const unsigned t0 = head + nv * VE;
     if (t0 + threadIdx.x < n) dst[t0 + threadIdx.x] = src[t0 + threadIdx.x];
 }
