@@ -765,7 +765,9 @@ def numba_reference(spec, sample):
             ok = bool(np.all(k[1:] >= k[:-1]))
         elif kind == "partition":
             a = sample[: 1 << 24].copy()
-            piv = float(a[vexsort.select_pivot(a, 0, len(a) - 1)])
+            from vexsort.quicksort import select_pivot as ref_select_pivot
+
+            piv = float(a[ref_select_pivot(a, 0, len(a) - 1)])
             vexsort.partition_region(a[: 1 << 12].copy(), piv)
             t0 = time.perf_counter()
             b = vexsort.partition_region(a, piv)
