@@ -487,9 +487,10 @@ __device__ __forceinline__ void plan_sort_samples(K* s, unsigned S) {
 // segment, or (n <= the finish capacity) one finish item whose source is the
 // input (root_flags bit0).
 __global__ void qs_init_kernel(Seg* segs, Ctl* ctl, Fin* fins, unsigned long long n, unsigned as_fin,
-                               unsigned root_flags) {
+                               unsigned root_flags, unsigned* presort_flags) {
     unsigned* w = reinterpret_cast<unsigned*>(ctl);
     for (unsigned i = threadIdx.x; i < 3 * sizeof(Ctl) / 4; i += blockDim.x) w[i] = 0u;
+    if (threadIdx.x < 2) presort_flags[threadIdx.x] = 0u;  // presort.cuh (the tile map's first words, free until the plan)
     __syncthreads();
     if (threadIdx.x == 0) {
         if (as_fin) {

@@ -22,6 +22,7 @@
 #include "local.cuh"
 #include "local2.cuh"
 #include "local3.cuh"
+#include "presort.cuh"
 
 using namespace vx;
 
@@ -232,6 +233,7 @@ struct SortCtx {
     uint64_t n, seed, ql_target, ql_cap;
     unsigned cap_seg, cap_spl, cap_bkt, cap_tiles, cap_fin, leaf, as_fin, root_flags, strategy, flags;
     int sms, g_hist, g_scat, g_fin, g_loc, g_seg;
+    bool presort;        // large sort: monotone inputs leave before level 0 (presort.cuh)
     bool global_local;   // CTA-local level with the intermediate in global memory (local.cuh)
     bool group_local;    // CTA-local level with lane-group networks over a padded stage (local2.cuh)
 };
@@ -254,6 +256,16 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
     const bool fin_only = x.as_fin && kind == LK_ROOT;
     if (fin_only) kernels = 1;
     if (!fin_only) {
+    if (kind == LK_ROOT && x.presort) {
+        // already ordered (or reverse ordered) input: found and finished here,
+        // the level's other kernels then see an empty queue
+        Launch l(KC_FINISH, st, timed ? 2 : 0, timed);
+        qs_presort_check_kernel<K, V><<<4 * x.sms, kPreNT, 0, st>>>(x.in_k, x.in_v, x.keys, x.vals, x.n, x.towner);
+        qs_presort_apply_kernel<K, V><<<4 * x.sms, kPreNT, 0, st>>>(x.keys, x.vals, x.in_k == x.keys ? 1 : 0, x.n,
+                                                                     x.towner, c);
+        kernels += 2;
+    }
+    VX_LAUNCHED();
     {
         Launch l(KC_PLAN, st, timed ? 1 : 0, timed);
         qs_plan_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(src_k, x.segs[p], c, x.spl, x.bkt, x.towner, x.cap_spl,
@@ -313,7 +325,7 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
 
 template <typename K, typename V>
 int launch_init(const SortCtx<K, V>& x, cudaStream_t st) {
-    qs_init_kernel<<<1, 64, 0, st>>>(x.segs[0], x.ctl, x.fins[0], x.n, x.as_fin, x.root_flags);
+    qs_init_kernel<<<1, 64, 0, st>>>(x.segs[0], x.ctl, x.fins[0], x.n, x.as_fin, x.root_flags, x.towner);
     VX_LAUNCHED();
     return VX_OK;
 }
@@ -627,6 +639,14 @@ int run_sort(const K* in_k, const V* in_v, K* keys, V* vals, uint64_t n, const v
     x.root_scr_k = x.as_fin ? in_k : x.sk;
     x.root_scr_v = x.as_fin ? in_v : x.sv;
 
+    {
+        // monotone-input check from 2^24 keys (two extra launches, ~6 us when
+        // the sampled pairs disagree, against a 0.37 ms sort at 2^24)
+        static const char* off = getenv("VX_NO_PRESORT");
+        static const char* mn = getenv("VX_PRESORT_MIN_N");
+        const uint64_t min_n = mn ? strtoull(mn, nullptr, 0) : (1ull << 24);
+        x.presort = !off && !x.as_fin && n >= min_n && n > 2 * kPreSample;
+    }
     x.sms = num_sms();
     x.g_hist = x.sms * VX_OCC(qs_hist_kernel<K>, kQsNT, hist_smem_bytes<K>());
     x.g_scat = x.sms * VX_OCC((qs_scatter_kernel<K, V>), kQsNT, sizeof(ScatterPipeSmem<K, V>));

@@ -752,3 +752,73 @@ def test_host_submit_wait_pairs_out_of_place():
         assert np.array_equal(k[dv.numpy()], dk.numpy())
         assert np.array_equal(np.sort(dv.numpy()), v)
     L.vx_host_release()
+
+
+# ------------------------------------------- monotone inputs (presort.cuh)
+
+
+def _stats_sort_into(src, **kw):
+    out = torch.empty_like(src)
+    st = {}
+    vx.sort_into(src, out, stats=st, **kw)
+    return out, st
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_monotone_inputs_leave_before_level_0(dt):
+    """Sorted and reverse-sorted inputs from 2^24 keys are recognised (one
+    read pass) and copied / reversed instead of partitioned; the output is
+    np.sort's either way, in place and out of place."""
+    n = (1 << 24) + 77
+    base = np.sort(inputs.c5_input(dt, "uniform", n=1 << 25)[:n])
+    for name, x in (("sorted", base), ("reverse", base[::-1].copy()), ("equal", np.full(n, 7, dtype=dt))):
+        t = _d(x)
+        out, st = _stats_sort_into(t)
+        assert st["scatter_elems"] == 0 and st["local_elems"] == 0 and st["finish_elems"] == n, (name, st)
+        assert torch.equal(t, _d(x)), "input of an out-of-place sort was modified"
+        assert np.array_equal(_h(out), base if name != "equal" else x), name
+        vx.sort(t)  # in place
+        assert np.array_equal(_h(t), base if name != "equal" else x), name
+
+
+def test_almost_monotone_inputs_still_sort():
+    """One inversion anywhere -- first pair, last pair, a CTA chunk boundary,
+    between the sampled pairs -- sends the sort down the normal path."""
+    n = 1 << 24
+    base = np.sort(inputs.c5_input(np.int32, "uniform", n=n))
+    rng = np.random.default_rng(8)
+    spots = [0, n - 2, n // 2, (n - 1) // 592, 12345677] + rng.integers(0, n - 1, size=3).tolist()
+    for rev in (False, True):
+        for p in spots:
+            x = base[::-1].copy() if rev else base.copy()
+            if x[p] == x[p + 1]:
+                continue
+            x[p], x[p + 1] = x[p + 1], x[p]
+            out, st = _stats_sort_into(_d(x))
+            assert st["scatter_elems"] > 0, (rev, p)
+            assert np.array_equal(_h(out), base), (rev, p)
+
+
+def test_monotone_pairs_and_plateaus():
+    """Key/value sorts: non-decreasing keys keep their pairs where they are,
+    non-increasing keys (plateaus of equal keys included) are reversed with
+    their values."""
+    n = 1 << 24
+    k = np.sort(np.random.default_rng(4).integers(0, 1 << 20, size=n).astype(np.int32))
+    v = np.arange(n, dtype=np.int32)
+    for keys in (k, k[::-1].copy()):
+        tk, tv = _d(keys), _d(v)
+        ok, ov = torch.empty_like(tk), torch.empty_like(tv)
+        st = {}
+        vx.sort_into(tk, ok, values=tv, out_values=ov, stats=st)
+        assert st["scatter_elems"] == 0, st
+        gk, gv = _h(ok), _h(ov)
+        assert np.array_equal(gk, k) and np.array_equal(keys[gv], gk)
+        assert np.array_equal(np.sort(gv), v)
+        vx.kv_sort(tk, tv)
+        assert np.array_equal(_h(tk), k) and np.array_equal(keys[_h(tv)], k)
+    kf = np.sort(np.random.default_rng(5).standard_normal(n))[::-1].copy()
+    vf = np.arange(n, dtype=np.int64)
+    tk, tv = _d(kf), _d(vf)
+    vx.kv_sort(tk, tv)
+    assert np.array_equal(_h(tk), kf[::-1]) and np.array_equal(kf[_h(tv)], kf[::-1])
