@@ -84,7 +84,9 @@ struct Seg {
     unsigned long long start, len;
     unsigned spl_off, m, bkt_off, tile_base;
     unsigned long long lo, hi;  // key-code bounds (lo > hi: unknown)
-    unsigned nb, shift, mode, mul;
+    unsigned nb;
+    unsigned direct;  // set by emit: every bucket is final, the scatter writes straight into the output
+    unsigned mode, mul;
     double vlo, vinv;  // mode 2
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
@@ -648,7 +650,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 segs[s].bkt_off = bo;
                 segs[s].tile_base = to;
                 segs[s].nb = nb;
-                segs[s].shift = 0;
+                segs[s].direct = 0;
                 segs[s].mul = mul;
                 segs[s].mode = sizeof(K) == 4 ? 1 : 2;
                 segs[s].vlo = vlo;
@@ -704,7 +706,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             segs[s].bkt_off = bo;
             segs[s].tile_base = to;
             segs[s].nb = 2 * m + 1;
-            segs[s].shift = 0;
+            segs[s].direct = 0;
             segs[s].mode = 0;
         }
         __syncthreads();
@@ -780,7 +782,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                                                           Fin* __restrict__ fins, unsigned cap_seg, unsigned cap_fin,
                                                           int dst_is_scratch, const K* __restrict__ spl_pool,
                                                           QlItemT* __restrict__ qls,
-                                                          uint64_t ql_cap) {
+                                                          uint64_t ql_cap, int direct_ok) {
     static_assert(kPlanNT >= kMaxBkt, "one thread per bucket");
     constexpr uint32_t LOCAL = FinCap<K, V>::value;
     __shared__ unsigned long long s_scan[kPlanNT / 32];
@@ -793,6 +795,14 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
         const unsigned b = threadIdx.x;
         const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + b] : 0ull;
         const unsigned long long ex = block_excl_scan_u64<kPlanNT>(c, s_scan);
+        // a bucket is final when it holds one key, one code (equal-width) or
+        // the keys equal to a pivot.  If EVERY bucket of the segment is final
+        // (few distinct keys) and the scatter may write the output (level 0 of
+        // an out-of-place sort: direct_ok), it does so and nothing is copied
+        // home afterwards.
+        const bool final_b = c == 1 || (sg.mode == 1 ? (sg.mul == 0) : sg.mode == 0 && (b & 1u) != 0);
+        const bool direct = !__syncthreads_or(b < nb && c > 0 && !final_b) && direct_ok != 0;
+        if (direct && threadIdx.x == 0) segs[s].direct = 1u;
         if (b < nb) {
             const unsigned long long bstart = sg.start + ex;
             bkt_pool[sg.bkt_off + b] = bstart;  // becomes the scatter cursor
@@ -843,9 +853,9 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                 chi = (unsigned long long)OKey<K>::of(spl_pool[sg.spl_off + j]) - 1;
             }
             if (c > 0) {
-                const bool final_ = c == 1 || (sg.mode == 1 ? (sg.mul == 0) : sg.mode == 0 && (b & 1u) != 0);
+                const bool final_ = final_b;
                 if (final_) {
-                    if (dst_is_scratch) {  // final but parked in scratch: copy home in chunks
+                    if (dst_is_scratch && !direct) {  // final but parked in scratch: copy home in chunks
                         // (this thread writes every chunk record: at most ~1024 per bucket)
                         const unsigned long long chunk =
                             max((unsigned long long)kCopyChunk, ((c >> 10) + 4095ull) & ~4095ull);

@@ -48,7 +48,7 @@ __device__ __forceinline__ void stage_writeout(const typename ScatterPipeSmem<K,
 template <typename K, typename V>
 __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K* __restrict__ src_k, const V* __restrict__ src_v,
                                                            const unsigned short* __restrict__ ids,
-                                                           K* __restrict__ dst_k, V* __restrict__ dst_v,
+                                                           K* __restrict__ dst_k, V* __restrict__ dst_v, K* root_out_k, V* root_out_v,
                                                            const Seg* __restrict__ segs, Ctl* __restrict__ ctl,
                                                            const unsigned* __restrict__ tile_owner,
                                                            unsigned long long* __restrict__ bkt_pool) {
@@ -61,6 +61,12 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     const unsigned t0 = (unsigned)(((uint64_t)blockIdx.x * ntiles) / gridDim.x);
     const unsigned t1 = (unsigned)(((uint64_t)(blockIdx.x + 1) * ntiles) / gridDim.x);
     if (t0 >= t1) return;
+    // level 0 of an out-of-place sort whose buckets are all final (emit set
+    // Seg::direct on the one root segment): straight into the output
+    if (root_out_k && segs[0].direct) {
+        dst_k = root_out_k;
+        dst_v = root_out_v;
+    }
     const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;  // the two buckets this thread scans / reserves
     const bool owner = b1 <= (unsigned)kMaxBkt;        // threads past the bucket range own none
     if (owner) sm.cnt[0][b0] = sm.cnt[0][b1] = sm.cnt[1][b0] = sm.cnt[1][b1] = 0u;

@@ -282,13 +282,15 @@ int launch_level(const SortCtx<K, V>& x, LevelKind kind, cudaStream_t st, cudaGr
     {
         Launch l(KC_EMIT, st, timed ? 1 : 0, timed);
         qs_emit_kernel<K, V><<<g_seg, kPlanNT, 0, st>>>(x.segs[p], c, nx, x.segs[p ^ 1], x.bkt, x.fins[p],
-                                                         x.cap_seg, x.cap_fin, p ? 0 : 1, x.spl, x.qls, x.ql_cap);
+                                                         x.cap_seg, x.cap_fin, p ? 0 : 1, x.spl, x.qls, x.ql_cap,
+                                                         kind == LK_ROOT && x.in_k != x.keys ? 1 : 0);
     }
     VX_LAUNCHED();
     {
         Launch l(KC_SCATTER, st, timed ? 1 : 0, timed);
         qs_scatter_kernel<K, V><<<x.g_scat, kQsNT, sizeof(ScatterPipeSmem<K, V>), st>>>(
-            src_k, src_v, x.ids, dst_k, dst_v, x.segs[p], c, x.towner, x.bkt);
+            src_k, src_v, x.ids, dst_k, dst_v, kind == LK_ROOT && x.in_k != x.keys ? x.keys : nullptr,
+            kind == LK_ROOT && x.in_k != x.keys ? x.vals : nullptr, x.segs[p], c, x.towner, x.bkt);
     }
     VX_LAUNCHED();
     if (x.ql_cap) {

@@ -822,3 +822,28 @@ def test_monotone_pairs_and_plateaus():
     tk, tv = _d(kf), _d(vf)
     vx.kv_sort(tk, tv)
     assert np.array_equal(_h(tk), kf[::-1]) and np.array_equal(kf[_h(tv)], kf[::-1])
+
+
+@pytest.mark.parametrize("dt", [np.int32, np.float64])
+def test_few_unique_scatters_straight_into_the_output(dt):
+    """Every level-0 bucket of a few-unique input is final (keys equal to a
+    pivot): an out-of-place sort scatters them straight into the output --
+    no copy home -- and an in-place sort still copies them back."""
+    n = (1 << 23) + 5
+    x = inputs.c5_input(dt, "few", n=1 << 24)[:n]
+    want = np.sort(x)
+    t = _d(x)
+    out, st = _stats_sort_into(t)
+    assert st["scatter_elems"] == n and st["finish_elems"] == 0 and st["levels"] == 1, st
+    assert np.array_equal(_h(out), want) and torch.equal(t, _d(x))
+    st2 = {}
+    vx.sort_into(t, t, stats=st2)  # in place: level 0 parks the buckets in scratch
+    assert st2["scatter_elems"] == n and st2["finish_elems"] == n, st2
+    assert np.array_equal(_h(t), want)
+    # pairs travel with their keys
+    k = _d(x)
+    v = torch.arange(n, dtype=torch.int32 if dt is np.int32 else torch.int64, device=DEV)
+    ok, ov = torch.empty_like(k), torch.empty_like(v)
+    vx.sort_into(k, ok, values=v, out_values=ov)
+    assert np.array_equal(_h(ok), want) and np.array_equal(x[_h(ov)], want)
+    assert np.array_equal(np.sort(_h(ov)), np.arange(n))
