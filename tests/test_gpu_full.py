@@ -264,3 +264,32 @@ def test_opt_in_variants_still_sort(env):
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, env: "1", "PYTHONPATH": root},
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_sorted_and_reverse_through_the_partition_levels():
+    """VX_NO_PRESORT switches the monotone-input shortcut off: sorted and
+    reverse inputs then take the partition levels (one-writer-per-bucket
+    scatter, equal-width levels, CTA-local level), as they did before the
+    shortcut existed -- still the same output."""
+    import subprocess
+    import sys
+
+    code = (
+        "import torch, paper_1704_08579_b200 as vx\n"
+        "from paper_1704_08579_b200.verify import generate, verify_sorted_permutation\n"
+        "for tdt, n in ((torch.int32, (1 << 27) + 9), (torch.float64, (1 << 26) + 3)):\n"
+        "    for dist in ('sorted', 'reverse'):\n"
+        "        src = generate(tdt, dist, n, seed=3)\n"
+        "        out = torch.empty_like(src)\n"
+        "        st = {}\n"
+        "        vx.sort_into(src, out, stats=st)\n"
+        "        verify_sorted_permutation(src, out)\n"
+        "        assert st['scatter_elems'] >= n, st\n"
+        "        want = src if dist == 'sorted' else torch.flip(src, [0])\n"
+        "        assert torch.equal(out, want)\n"
+        "print('ok')\n"
+    )
+    root = os.path.dirname(HERE)
+    r = subprocess.run([sys.executable, "-c", code], env={**os.environ, "VX_NO_PRESORT": "1", "PYTHONPATH": root},
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
