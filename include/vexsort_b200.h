@@ -86,6 +86,12 @@ int vx_version(void);
  * NULL).  Replaces _kernels.quicksort / kv_quicksort (_kernels.py:378-482)
  * as called by sort_with_config (quicksort.py:115-134) and kv_sort
  * (keyvalue.py:228-252). */
+/* Inputs that are already in order leave early: a sort of >= 2^24 keys first
+ * tests 2048 evenly spaced adjacent pairs and, only if all of them rise (or
+ * all fall), every adjacent pair in one read pass; a non-decreasing array is
+ * then copied (or left in place), a non-increasing one written reversed
+ * (csrc/presort.cuh; environment VX_NO_PRESORT switches the test off,
+ * VX_PRESORT_MIN_N moves the threshold).  The output is the same either way. */
 size_t vx_sort_workspace_bytes(int dtype, int has_values, int64_t n);
 int vx_sort(int dtype, void *keys, void *values, int64_t n, const vx_sort_config *cfg, void *ws,
             size_t ws_bytes, vx_stream_t stream);

@@ -23,5 +23,5 @@ echo "summarize rc=$?"
 cp profiles/ncu_summary_$TAG.md profiles/ncu_traffic.json gpurun_out/art/ 2>/dev/null
 cp gpurun_out/prof/launches_default.csv gpurun_out/art/launches_default_$TAG.csv
 for w in sort_i32 sort_f64 c4 c3 c2_i32; do python tools/ncu_stalls.py gpurun_out/prof/full_$w.ncu-rep > gpurun_out/art/stalls_$w.txt 2>&1; done
-mv gpurun_out/prof/full_sort_i32.ncu-rep gpurun_out/art/full_sort_i32_$TAG.ncu-rep
+# (the .ncu-rep files stay on the box: gpurun brings back at most 64 MiB)
 rm -rf gpurun_out/prof gpurun_out/all gpurun_out/quick gpurun_out/traffic
