@@ -87,7 +87,7 @@ int vx_version(void);
  * as called by sort_with_config (quicksort.py:115-134) and kv_sort
  * (keyvalue.py:228-252). */
 /* Inputs that are already in order leave early: a sort of >= 2^24 keys first
- * tests 2048 evenly spaced adjacent pairs and, only if all of them rise (or
+ * tests 512 evenly spaced adjacent pairs and, only if all of them rise (or
  * all fall), every adjacent pair in one read pass; a non-decreasing array is
  * then copied (or left in place), a non-increasing one written reversed
  * (csrc/presort.cuh; environment VX_NO_PRESORT switches the test off,

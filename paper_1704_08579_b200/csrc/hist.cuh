@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     }
     __syncthreads();
 
-    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, rsh = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, rsh = 0, cs = 0;
     bool radix = false, vmode = false;
     U rlo = 0;
     double vlo = 0.0, vinv = 0.0;
@@ -122,11 +122,12 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             __syncthreads();
             if (cur != 0xffffffffu)
                 for (unsigned b = tid; b < nb; b += kQsNT)
-                    if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+                    if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + (b << cs)], (unsigned long long)s_hist[b]);
             cur = bt.seg;
             const Seg sg = segs[bt.seg];
             bkt_off = sg.bkt_off;
             nb = sg.nb;
+            cs = sg.cshift;
             radix = sg.mode == 1;
             vmode = sg.mode == 2;
             vlo = sg.vlo;
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
     }
     __syncthreads();
     for (unsigned b = tid; b < nb; b += kQsNT)
-        if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + b], (unsigned long long)s_hist[b]);
+        if (s_hist[b]) atomicAdd(&bkt_pool[bkt_off + (b << cs)], (unsigned long long)s_hist[b]);
 }
 
 }  // namespace vx

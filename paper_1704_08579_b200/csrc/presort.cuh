@@ -4,9 +4,9 @@
 // sorted input (finding 5); the partition levels here are
 // not, but they still move every key three times to arrive where it started.
 // Large sorts therefore first ask whether the input is monotone:
-//   * qs_presort_check_kernel: every CTA tests 2048 evenly spaced adjacent
+//   * qs_presort_check_kernel: every CTA tests 512 evenly spaced adjacent
 //     pairs (a few microseconds; random data fails here with certainty
-//     1 - 2^-2048 and the kernel returns); if all of them rise (or all fall)
+//     1 - 2^-512 and the kernel returns); if all of them rise (or all fall)
 //     the CTAs test EVERY adjacent pair of their chunk of the array -- one
 //     read pass, which an out-of-place sort also uses to write the copy (or
 //     the reversed copy: pairs travel together and equal keys may take any
@@ -24,7 +24,7 @@
 namespace vx {
 
 constexpr int kPreNT = 512;
-constexpr unsigned kPreSample = 2048;
+constexpr unsigned kPreSample = 512;  // one pair per thread: a single round of loads
 
 // 1: the sampled adjacent pairs never fall; 2: they never rise; 0: neither.
 template <typename K>

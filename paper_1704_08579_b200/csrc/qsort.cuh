@@ -51,6 +51,19 @@ constexpr int kFinNT = 512;                    // finish-kernel threads
 constexpr int kMaxSample = 4096;
 constexpr int kFinSample = 1024;
 constexpr uint32_t kCopyChunk = 16384;
+// Bucket b of a segment counts (histogram) and reserves its runs (scatter)
+// at bkt_pool[bkt_off + (b << cshift)].  Every tile of a level hits these
+// cursors with one atomic per bucket, and L2 serialises atomics that share a
+// 32-byte sector.  The equal-width ROOT level has a few hundred cursors side
+// by side that every CTA of the GPU hammers: four per sector cost the 2^32
+// int32 sort 7.7 ms (scatter 40.2 vs 32.5 ms), so they sit four slots apart,
+// one per sector.  Later levels spread their atomics over hundreds of
+// segments; spacing their cursors out only costs cache lines (measured: +1.1
+// ms), and a sampled level's range buckets already sit two apart.
+#ifndef VX_ROOT_CSHIFT
+#define VX_ROOT_CSHIFT 2
+#endif
+constexpr unsigned kRootBktSlots = 512u << VX_ROOT_CSHIFT;  // pool slots the root level may take
 constexpr int kMaxLevels = 48;
 constexpr double kQlSlack = 2.0;  // global levels aim CTA-local leaves at <= this x the target
 
@@ -88,6 +101,7 @@ struct Seg {
     unsigned direct;  // set by emit: every bucket is final, the scatter writes straight into the output
     unsigned mode, mul;
     double vlo, vinv;  // mode 2
+    unsigned cshift, pad_;  // bucket b's counter / cursor is bkt_pool[bkt_off + (b << cshift)]
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -617,10 +631,9 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             mt = (unsigned)max(2.0, min((double)kMaxSplit, f - 1.0));
             rb = (unsigned)max(2.0, min((double)kMaxBkt, f));
         }
-        if (radix) {
-            // bounds known from the parent: rb equal-width buckets over
-            // [lo, hi] -- no sample, no pivot table
-            const uint64_t range = (uint64_t)(U)(shi - slo);
+        // rb equal-width buckets over the code bounds [blo, bhi] -- no pivot table
+        auto equal_width = [&](uint64_t blo, uint64_t bhi, unsigned cs) {
+            const uint64_t range = (uint64_t)(U)(bhi - blo);
             unsigned nb = rb;
             unsigned mul = 0;
             double vlo = 0.0, vinv = 0.0;
@@ -629,15 +642,15 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 else mul = (unsigned)(((uint64_t)nb << 32) / (range + 1));
             } else {
                 // value space: x in [vlo, vhi] -> trunc((x - vlo) * vinv) in [0, nb)
-                vlo = ord_to_f64((uint64_t)slo);
-                const double w = ord_to_f64((uint64_t)shi) - vlo;  // > 0 (slo < shi; -0.0 / +0.0 aside)
+                vlo = ord_to_f64((uint64_t)blo);
+                const double w = ord_to_f64((uint64_t)bhi) - vlo;  // > 0 (blo < bhi; -0.0 / +0.0 aside)
                 vinv = w > 0.0 && w < 1.7e308 ? (double)nb * (1.0 - 1e-12) / w : 0.0;  // 0: everything in bucket 0
             }
             if (threadIdx.x == 0) {
                 const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
-                unsigned bo = atomicAdd(&ctl->bkt_ctr, nb);
+                unsigned bo = atomicAdd(&ctl->bkt_ctr, nb << cs);
                 unsigned to = atomicAdd(&ctl->tile_ctr, ntiles);
-                if (bo + nb > cap_bkt || to + ntiles > cap_tiles) {
+                if (bo + (nb << cs) > cap_bkt || to + ntiles > cap_tiles) {
                     // capacity exceeded: flag it; hist / emit / scatter skip the
                     // level (they test ctl->err), so no pool slot is aliased
                     atomicOr(&ctl->err, kErrCapacity);
@@ -655,16 +668,28 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 segs[s].mode = sizeof(K) == 4 ? 1 : 2;
                 segs[s].vlo = vlo;
                 segs[s].vinv = vinv;
+                segs[s].lo = blo;
+                segs[s].hi = bhi;
+                segs[s].cshift = cs;
             }
             __syncthreads();
-            for (unsigned b = threadIdx.x; b < nb; b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
+            for (unsigned b = threadIdx.x; b < (nb << cs); b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
             const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
             for (unsigned t = threadIdx.x; t < ntiles; t += kPlanNT) tile_owner[s_off[2] + t] = s;
             __syncthreads();
+        };
+        if (radix) {
+            // bounds known from the parent: no sample either
+            equal_width(slo, shi, 0u);
             continue;
         }
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
+#ifndef VX_NO_UNIFORM_ROOT
+        // the whole array of a large sort of 4-byte keys: the full sample, so
+        // the uniformity test below has its 4 sigma
+        if (sizeof(K) == 4 && nseg == 1 && tot->level == 0 && len >= (1ull << 24)) S = kMaxSample;
+#endif
 #pragma unroll 4
         for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
             s_samp[i] = src[start + sample_pos(strategy, seed, start, len, i, S)];
@@ -674,6 +699,35 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         cta_bitonic<K, NoVal, kPlanNT>(s_samp, nullptr, S);
 #else
         plan_sort_samples<K>(s_samp, S);
+#endif
+#ifndef VX_NO_UNIFORM_ROOT
+        if constexpr (sizeof(K) == 4) {
+            // 4-byte keys spread evenly over the whole code range (hashes,
+            // random ids, the C1 / C5 uniform inputs): equal-width buckets over
+            // the type's bounds instead of sampled pivots -- the histogram pass
+            // then classifies with a high multiply instead of the cell table
+            // and a splitter compare (2^28: 0.52 -> 0.35 ms).  Decided on the
+            // sorted sample: every 64th-quantile within 2^27 codes (3 % of the
+            // range, 4 sigma of a 4096-key sample) of where a uniform
+            // distribution puts it.  Anything else -- narrower ranges,
+            // clusters, few distinct keys -- keeps the sampled pivots; a
+            // distribution that passes and still fills some bucket beyond the
+            // leaf capacity just costs that bucket one more level.
+            bool uni = S == (unsigned)kMaxSample && rb >= 2;
+            if (threadIdx.x >= 1 && threadIdx.x < 64) {
+                const uint32_t got = (uint32_t)OKey<K>::of(s_samp[threadIdx.x * (S / 64)]);
+                const uint32_t want = threadIdx.x << 26;
+                const uint32_t dev = got > want ? got - want : want - got;
+                uni = uni && dev <= (1u << 27);
+            }
+            if (__syncthreads_and(uni)) {
+#ifndef VX_UNIFORM_ROOT_WIDE
+                rb = min(rb, mt + 1);  // the fan-out the sampled level would have had
+#endif
+                equal_width(0ull, 0xffffffffull, (unsigned)VX_ROOT_CSHIFT);
+                continue;
+            }
+        }
 #endif
         // candidate j = sample at quantile (j+1)/(mt+1); keep distinct values
         K cand = K();
@@ -692,9 +746,10 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         if (threadIdx.x == 0) {
             const unsigned ntiles = (unsigned)((len + TILE - 1) / TILE);
             unsigned so = atomicAdd(&ctl->spl_ctr, m);
-            unsigned bo = atomicAdd(&ctl->bkt_ctr, 2 * m + 1);
+            constexpr unsigned cs = 0;
+            unsigned bo = atomicAdd(&ctl->bkt_ctr, (2 * m + 1) << cs);
             unsigned to = atomicAdd(&ctl->tile_ctr, ntiles);
-            if (so + m > cap_spl || bo + 2 * m + 1 > cap_bkt || to + ntiles > cap_tiles) {
+            if (so + m > cap_spl || bo + ((2 * m + 1) << cs) > cap_bkt || to + ntiles > cap_tiles) {
                 atomicOr(&ctl->err, kErrCapacity);
                 so = bo = to = 0;
             }
@@ -708,6 +763,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             segs[s].nb = 2 * m + 1;
             segs[s].direct = 0;
             segs[s].mode = 0;
+            segs[s].cshift = cs;
         }
         __syncthreads();
         if (keep) spl_pool[s_off[0] + rank] = cand;
@@ -793,7 +849,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
         const unsigned nb = sg.nb;
         const bool radix = sg.mode != 0;
         const unsigned b = threadIdx.x;
-        const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + b] : 0ull;
+        const unsigned long long c = b < nb ? bkt_pool[sg.bkt_off + (b << sg.cshift)] : 0ull;
         const unsigned long long ex = block_excl_scan_u64<kPlanNT>(c, s_scan);
         // a bucket is final when it holds one key, one code (equal-width) or
         // the keys equal to a pivot.  If EVERY bucket of the segment is final
@@ -805,7 +861,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
         if (direct && threadIdx.x == 0) segs[s].direct = 1u;
         if (b < nb) {
             const unsigned long long bstart = sg.start + ex;
-            bkt_pool[sg.bkt_off + b] = bstart;  // becomes the scatter cursor
+            bkt_pool[sg.bkt_off + (b << sg.cshift)] = bstart;  // becomes the scatter cursor
             // the bucket's key-code bounds, for the child's own partition:
             // a range bucket 2j lies strictly between pivots j-1 and j; a
             // radix bucket spans its 2^shift codes.  A radix child holding

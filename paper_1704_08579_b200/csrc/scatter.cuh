@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     const unsigned b0 = 2 * threadIdx.x, b1 = b0 + 1;  // the two buckets this thread scans / reserves
     const bool owner = b1 <= (unsigned)kMaxBkt;        // threads past the bucket range own none
     if (owner) sm.cnt[0][b0] = sm.cnt[0][b1] = sm.cnt[1][b0] = sm.cnt[1][b1] = 0u;
-    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0;
+    unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, cs = 0;
     TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
     K k[IPT];
     V v[IPT];
@@ -96,6 +96,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
             cur = g.seg;
             bkt_off = segs[g.seg].bkt_off;
             nb = segs[g.seg].nb;
+            cs = segs[g.seg].cshift;
         }
         unsigned* cnt = sm.cnt[p];
         moved += g.tn;
@@ -132,8 +133,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         unsigned tot;
         const unsigned ex = block_excl_scan<kQsNT>(c0 + c1, sm.scan, &tot);
         unsigned long long r0 = 0, r1 = 0;
-        if (c0) r0 = atomicAdd(&bkt_pool[bkt_off + b0], (unsigned long long)c0);
-        if (c1) r1 = atomicAdd(&bkt_pool[bkt_off + b1], (unsigned long long)c1);
+        if (c0) r0 = atomicAdd(&bkt_pool[bkt_off + (b0 << cs)], (unsigned long long)c0);
+        if (c1) r1 = atomicAdd(&bkt_pool[bkt_off + (b1 << cs)], (unsigned long long)c1);
         if (b0 < nb) cnt[b0] = ex;
         if (b1 < nb) cnt[b1] = ex + c0;
         if (threadIdx.x == 0) S.tn = g.tn;

@@ -106,9 +106,9 @@ struct SortLayout {
         constexpr bool KV = HasVal<V>::value;
         cap_seg = n / (LOCAL + 1) + 2;
         cap_spl = 2 * n / LOCAL + 2 * cap_seg + 512;
-        cap_bkt = 2 * cap_spl + cap_seg;
+        cap_bkt = std::max<uint64_t>(2 * cap_spl + cap_seg, kRootBktSlots);  // (the root's cursors are spaced out)
         cap_tiles = n / TILE + cap_seg + 1;
-        cap_fin = 2 * cap_bkt + n / kCopyChunk + 16;
+        cap_fin = 2 * (2 * cap_spl + cap_seg) + n / kCopyChunk + 16;
         static_assert(3 * sizeof(Ctl) <= kCtlBytes, "control records");
         size_t o = 0;
         off_ctl = o; o = align_up(o + kCtlBytes);
