@@ -101,7 +101,8 @@ struct Seg {
     unsigned direct;  // set by emit: every bucket is final, the scatter writes straight into the output
     unsigned mode, mul;
     double vlo, vinv;  // mode 2
-    unsigned cshift, pad_;  // bucket b's counter / cursor is bkt_pool[bkt_off + (b << cshift)]
+    unsigned cshift;  // bucket b's counter / cursor is bkt_pool[bkt_off + (b << cshift)]
+    unsigned open;    // mode 2 root: [lo, hi] are the SAMPLE's extremes; keys beyond them sit in the edge buckets
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             rb = (unsigned)max(2.0, min((double)kMaxBkt, f));
         }
         // rb equal-width buckets over the code bounds [blo, bhi] -- no pivot table
-        auto equal_width = [&](uint64_t blo, uint64_t bhi, unsigned cs) {
+        auto equal_width = [&](uint64_t blo, uint64_t bhi, unsigned cs, unsigned open) {
             const uint64_t range = (uint64_t)(U)(bhi - blo);
             unsigned nb = rb;
             unsigned mul = 0;
@@ -671,6 +672,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 segs[s].lo = blo;
                 segs[s].hi = bhi;
                 segs[s].cshift = cs;
+                segs[s].open = open;
             }
             __syncthreads();
             for (unsigned b = threadIdx.x; b < (nb << cs); b += kPlanNT) bkt_pool[s_off[1] + b] = 0;
@@ -680,15 +682,15 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
         };
         if (radix) {
             // bounds known from the parent: no sample either
-            equal_width(slo, shi, 0u);
+            equal_width(slo, shi, 0u, 0u);
             continue;
         }
         unsigned S = next_pow2_u32(16 * (mt + 1));
         S = S < 256 ? 256 : (S > kMaxSample ? kMaxSample : S);
 #ifndef VX_NO_UNIFORM_ROOT
-        // the whole array of a large sort of 4-byte keys: the full sample, so
-        // the uniformity test below has its 4 sigma
-        if (sizeof(K) == 4 && nseg == 1 && tot->level == 0 && len >= (1ull << 24)) S = kMaxSample;
+        // the whole array of a large sort: the full sample, so the uniformity
+        // test below has its 4 sigma
+        if (nseg == 1 && tot->level == 0 && len >= (1ull << 24)) S = kMaxSample;
 #endif
 #pragma unroll 4
         for (unsigned i = threadIdx.x; i < S; i += kPlanNT) {
@@ -724,7 +726,28 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
 #ifndef VX_UNIFORM_ROOT_WIDE
                 rb = min(rb, mt + 1);  // the fan-out the sampled level would have had
 #endif
-                equal_width(0ull, 0xffffffffull, (unsigned)VX_ROOT_CSHIFT);
+                equal_width(0ull, 0xffffffffull, (unsigned)VX_ROOT_CSHIFT, 0u);
+                continue;
+            }
+        } else {
+            // float64: the same test in VALUE space over the sample's own
+            // extremes (there is no meaningful type range).  The few keys
+            // beyond them land in the first and last bucket -- the classifier
+            // saturates on both sides -- whose children therefore get no
+            // bounds (emit) and find their own.
+            const double smin = (double)s_samp[0], smax = (double)s_samp[S - 1], w = smax - smin;
+            bool uni = S == (unsigned)kMaxSample && rb >= 2 && w > 0.0 && w < 1.7e308;
+            if (threadIdx.x >= 1 && threadIdx.x < 64) {
+                const double got = (double)s_samp[threadIdx.x * (S / 64)];
+                const double want = smin + w * ((double)threadIdx.x * (1.0 / 64.0));
+                uni = uni && fabs(got - want) <= w * (1.0 / 32.0);
+            }
+            if (__syncthreads_and(uni)) {
+#ifndef VX_UNIFORM_ROOT_WIDE
+                rb = min(rb, mt + 1);
+#endif
+                equal_width((uint64_t)OKey<K>::of(s_samp[0]), (uint64_t)OKey<K>::of(s_samp[S - 1]),
+                            (unsigned)VX_ROOT_CSHIFT, 1u);
                 continue;
             }
         }
@@ -764,6 +787,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
             segs[s].direct = 0;
             segs[s].mode = 0;
             segs[s].cshift = cs;
+            segs[s].open = 0;
         }
         __syncthreads();
         if (keep) spl_pool[s_off[0] + rank] = cand;
@@ -885,6 +909,10 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                             if (b == 0) clo = sg.lo;
                             if (b + 1 == nb) chi = sg.hi;
                         }
+                    }
+                    if (sg.open && (b == 0 || b + 1 == nb)) {  // keys beyond the sample's extremes live here
+                        clo = 1;
+                        chi = 0;
                     }
                 }
                 if (2 * c > sg.len) {

@@ -847,3 +847,54 @@ def test_few_unique_scatters_straight_into_the_output(dt):
     vx.sort_into(k, ok, values=v, out_values=ov)
     assert np.array_equal(_h(ok), want) and np.array_equal(x[_h(ov)], want)
     assert np.array_equal(np.sort(_h(ov)), np.arange(n))
+
+
+def test_uniform_looking_samples_with_structure_underneath():
+    """Inputs whose coarse quantiles look uniform over the int32 range (so the
+    root level takes equal-width buckets) but which are not uniform below
+    that: a lattice of 4096 values, a heavy cluster, a narrow spike on a
+    uniform floor.  Skewed children fall back to sampled pivots; the output is
+    np.sort's."""
+    rng = np.random.default_rng(12)
+    n = (1 << 24) + 11
+    full = rng.integers(-(2**31), 2**31 - 1, size=n, dtype=np.int64, endpoint=True)
+    cases = {
+        "lattice": (full >> 20) << 20,
+        "cluster": np.where(rng.random(n) < 0.02, 123456789, full),
+        "spike": np.where(rng.random(n) < 0.03, 1000 + rng.integers(0, 64, size=n), full),
+        "pairs": (full >> 1) << 1,
+    }
+    for name, x in cases.items():
+        x = x.astype(np.int32)
+        out, st = _stats_sort_into(_d(x))
+        assert np.array_equal(_h(out), np.sort(x)), name
+        k = _d(x)
+        v = torch.arange(n, dtype=torch.int32, device=DEV)
+        vx.kv_sort(k, v)
+        assert np.array_equal(_h(k), np.sort(x)) and np.array_equal(x[_h(v)], _h(k)), name
+
+
+def test_uniform_looking_float64_with_outliers():
+    """float64 keys whose sample looks uniform between its own extremes (the
+    root level then cuts equal-width buckets in value space) with keys BEYOND
+    those extremes -- a handful of huge outliers, infinities, both zeros --
+    which saturate into the edge buckets; also a lattice and a normal
+    distribution (which fails the test and keeps sampled pivots)."""
+    rng = np.random.default_rng(21)
+    n = (1 << 24) + 3
+    u = rng.uniform(-1e6, 1e6, size=n)
+    out_idx = rng.choice(n, size=64, replace=False)
+    a = u.copy()
+    a[out_idx[:16]] = 1e12 * rng.uniform(1, 2, size=16)
+    a[out_idx[16:32]] = -1e12 * rng.uniform(1, 2, size=16)
+    a[out_idx[32:36]] = np.inf
+    a[out_idx[36:40]] = -np.inf
+    a[out_idx[40:44]] = 0.0
+    a[out_idx[44:48]] = -0.0
+    cases = {"outliers": a, "lattice": np.round(u / 512.0) * 512.0, "normal": rng.standard_normal(n),
+             "positive": rng.uniform(1e-300, 1e-290, size=n)}
+    for name, x in cases.items():
+        out, st = _stats_sort_into(_d(x))
+        got, want = _h(out), np.sort(x)
+        assert np.array_equal(got, want), name  # (+0.0 == -0.0 under array_equal; any order of the two is a sort)
+        assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(x.view(np.uint64))), name  # same bit patterns
