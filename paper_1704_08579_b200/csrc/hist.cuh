@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             if (vmode) return min(nb - 1, (unsigned)__double2uint_rz(((double)key - vlo) * vinv));
         }
         if (radix) {
-            const uint32_t d = (uint32_t)(OKey<K>::of(key) - rlo);
+            // (saturating below: an open-ended root sees keys under its lower bound)
+            const uint32_t d = (uint32_t)(max(OKey<K>::of(key), rlo) - rlo);
             return min(nb - 1, rsh ? __umulhi(d, rsh) : d);
         }
         return ct_classify(s_ct, cp, key);

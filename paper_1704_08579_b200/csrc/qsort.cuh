@@ -102,7 +102,7 @@ struct Seg {
     unsigned mode, mul;
     double vlo, vinv;  // mode 2
     unsigned cshift;  // bucket b's counter / cursor is bkt_pool[bkt_off + (b << cshift)]
-    unsigned open;    // mode 2 root: [lo, hi] are the SAMPLE's extremes; keys beyond them sit in the edge buckets
+    unsigned open;    // root over the SAMPLE's extremes [lo, hi]: keys beyond them sit in the edge buckets
 };
 struct QlItemT {  // a segment for the CTA-local level (local.cuh)
     unsigned long long start, len;
@@ -729,6 +729,25 @@ __global__ void __launch_bounds__(kPlanNT) qs_plan_kernel(const K* __restrict__ 
                 equal_width(0ull, 0xffffffffull, (unsigned)VX_ROOT_CSHIFT, 0u);
                 continue;
             }
+            // the same test over the SAMPLE's extremes (keys uniform over part
+            // of the range, e.g. C4's [0, 2^31)): the keys beyond them saturate
+            // into the first and last bucket, whose children get no bounds
+            const uint32_t smin = (uint32_t)OKey<K>::of(s_samp[0]), smax = (uint32_t)OKey<K>::of(s_samp[S - 1]);
+            const uint32_t w = smax - smin;
+            uni = S == (unsigned)kMaxSample && rb >= 2 && w >= (1u << 20);
+            if (threadIdx.x >= 1 && threadIdx.x < 64) {
+                const uint32_t got = (uint32_t)OKey<K>::of(s_samp[threadIdx.x * (S / 64)]);
+                const uint32_t want = smin + (uint32_t)(((uint64_t)w * threadIdx.x) >> 6);
+                const uint32_t dev = got > want ? got - want : want - got;
+                uni = uni && dev <= (w >> 5);
+            }
+            if (__syncthreads_and(uni)) {
+#ifndef VX_UNIFORM_ROOT_WIDE
+                rb = min(rb, mt + 1);
+#endif
+                equal_width((uint64_t)smin, (uint64_t)smax, (unsigned)VX_ROOT_CSHIFT, 1u);
+                continue;
+            }
         } else {
             // float64: the same test in VALUE space over the sample's own
             // extremes (there is no meaningful type range).  The few keys
@@ -927,7 +946,7 @@ __global__ void __launch_bounds__(kPlanNT) qs_emit_kernel(Seg* __restrict__ segs
                 };
                 clo = sg.lo + dlo(b);
                 chi = b + 1 < nb ? sg.lo + dlo(b + 1ull) - 1 : sg.hi;
-                if (2 * c > sg.len) {
+                if (2 * c > sg.len || (sg.open && (b == 0 || b + 1 == nb))) {
                     clo = 1;
                     chi = 0;
                 }
