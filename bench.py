@@ -860,6 +860,8 @@ def main():
     rank, world, local = dist_setup(args.gpus)
     r = run_ours(args, spec, rank, world, local)
     xname = "NCCL all-to-all" if spec.get("exchange") != "fused" else "fused partition + IPC/NVLink stores"
+    if os.environ.get("VX_BENCH_BACKEND", "nccl") != "nccl":
+        xname += f"; {os.environ['VX_BENCH_BACKEND']} collectives, host-staged: a functional check, not a measurement"
     cfg["parallelism"] = ((f"sample sort over {world} ranks ({xname})" if world > 1 else
                            "single GPU (P=1 sample sort = the local hybrid sort; no exchange)")
                           if spec["kind"] == "sharded"
