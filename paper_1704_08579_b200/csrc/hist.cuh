@@ -12,7 +12,10 @@
 // buckets) and counted in a shared histogram that is flushed to the
 // segment's global histogram once per (CTA, segment).  The bucket id of every
 // element is stored (u16, coalesced) for the scatter pass, which then ranks
-// and moves elements without classifying them again.
+// and moves elements without classifying them again -- except in equal-width
+// segments of 4-byte keys, where the scatter recomputes it (a subtract and a
+// high multiply) and this pass, DRAM-bound once its grid was chunked, writes
+// nothing.
 #pragma once
 
 #include "common.cuh"
@@ -139,6 +142,8 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
             for (unsigned b = tid; b < nb; b += kQsNT) s_hist[b] = 0;
             __syncthreads();
         }
+        // (the scatter recomputes the bucket of a 4-byte key in an equal-width segment)
+        const bool store_ids = sizeof(K) != 4 || !radix;
         const char* buf = reinterpret_cast<const char*>(smem_raw) + stage * BUF;
         if (bt.body == TILE) {  // the whole (full) tile is in shared memory
             const K* sb = reinterpret_cast<const K*>(buf + bt.shift);
@@ -149,7 +154,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                 // result unused: ATOMS.POPC.INC, which already merges the
                 // lanes of a warp that hit one counter (sorted inputs)
                 atomicAdd(&s_hist[b], 1u);
-                ids[bt.base + i * kQsNT + tid] = (unsigned short)b;
+                if (store_ids) ids[bt.base + i * kQsNT + tid] = (unsigned short)b;
             }
         } else {
 #pragma unroll
@@ -160,7 +165,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_hist_kernel(const K* _
                     const unsigned b = classify(x);
                     VX_ASSERT(b < nb && bt.base + idx < n_all);
                     atomicAdd(&s_hist[b], 1u);
-                    ids[bt.base + idx] = (unsigned short)b;
+                    if (store_ids) ids[bt.base + idx] = (unsigned short)b;
                 }
             }
         }

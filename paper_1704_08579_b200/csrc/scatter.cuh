@@ -71,12 +71,17 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
     const bool owner = b1 <= (unsigned)kMaxBkt;        // threads past the bucket range own none
     if (owner) sm.cnt[0][b0] = sm.cnt[0][b1] = sm.cnt[1][b0] = sm.cnt[1][b1] = 0u;
     unsigned cur = 0xffffffffu, bkt_off = 0, nb = 0, cs = 0;
+    // equal-width segments of 4-byte keys (mode 1): the histogram pass stores
+    // no ids for them; a key's bucket is a subtract and a high multiply away
+    // (2 B/key less to write there and to read here)
+    auto stored_ids = [&](unsigned seg) -> bool { return sizeof(K) != 4 || segs[seg].mode != 1; };
+    unsigned ew = 0, ew_lo = 0, ew_mul = 0;
     TileGeo g = tile_geo<TILE>(t0, tile_owner, segs);
     K k[IPT];
     V v[IPT];
     unsigned short id[IPT];
     load_tile<K, IPT>(k, src_k, g);
-    load_tile<unsigned short, IPT>(id, ids, g);
+    if (stored_ids(g.seg)) load_tile<unsigned short, IPT>(id, ids, g);
     if constexpr (KV) load_tile<V, IPT>(v, src_v, g);
     unsigned long long moved = 0;
     __syncthreads();
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
         if (t + 1 < t1) {
             gn = tile_geo<TILE>(t + 1, tile_owner, segs);
             load_tile<K, IPT>(kn, src_k, gn);
-            load_tile<unsigned short, IPT>(idn, ids, gn);
+            if (stored_ids(gn.seg)) load_tile<unsigned short, IPT>(idn, ids, gn);
             if constexpr (KV) load_tile<V, IPT>(vn, src_v, gn);
         }
         if (g.seg != cur) {
@@ -97,6 +102,20 @@ __global__ void __launch_bounds__(kQsNT, kQsMinBlocks) qs_scatter_kernel(const K
             bkt_off = segs[g.seg].bkt_off;
             nb = segs[g.seg].nb;
             cs = segs[g.seg].cshift;
+            if constexpr (sizeof(K) == 4) {
+                ew = segs[g.seg].mode == 1 ? 1u : 0u;
+                ew_lo = (unsigned)segs[g.seg].lo;
+                ew_mul = segs[g.seg].mul;
+            }
+        }
+        if constexpr (sizeof(K) == 4) {
+            if (ew) {
+#pragma unroll
+                for (int i = 0; i < IPT; ++i) {
+                    const uint32_t d = max((uint32_t)OKey<K>::of(k[i]), ew_lo) - ew_lo;
+                    id[i] = (unsigned short)min(nb - 1, ew_mul ? __umulhi(d, ew_mul) : d);
+                }
+            }
         }
         unsigned* cnt = sm.cnt[p];
         moved += g.tn;
