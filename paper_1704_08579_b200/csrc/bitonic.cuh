@@ -109,7 +109,19 @@ struct WarpBitonic {
                     mk = t ? pk : mk;
                     mv = t ? pv : mv;
                 } else {
-                    mk = low ? kmin(mk, pk) : kmax(mk, pk);
+                    if constexpr (std::is_floating_point<K>::value) {
+                        // +0.0 and -0.0 compare equal but are different keys.
+                        // min on the low lane and max on the high lane must
+                        // resolve that tie the same way -- both lanes keep their
+                        // own key -- or the high lane takes its partner's zero
+                        // and the pair ends up holding the same zero twice.
+                        // One ordered compare with the operands swapped on the
+                        // high lane: exchange iff (high lane's key) < (low lane's).
+                        const K hi_k = low ? pk : mk, lo_k = low ? mk : pk;
+                        mk = hi_k < lo_k ? pk : mk;
+                    } else {
+                        mk = low ? kmin(mk, pk) : kmax(mk, pk);
+                    }
                 }
             };
 #pragma unroll

@@ -898,3 +898,35 @@ def test_uniform_looking_float64_with_outliers():
         got, want = _h(out), np.sort(x)
         assert np.array_equal(got, want), name  # (+0.0 == -0.0 under array_equal; any order of the two is a sort)
         assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(x.view(np.uint64))), name  # same bit patterns
+
+
+def test_both_zeros_survive_every_network():
+    """+0.0 and -0.0 compare equal but are different keys: every sort path
+    (warp networks of the segment sort and the finish kernel, lane networks
+    of the CTA-local level) must return the input's multiset of BIT PATTERNS.
+    A cross-lane comparator that let the high lane take its partner on a tie
+    duplicated one zero and lost the other."""
+    rng = np.random.default_rng(33)
+    for n in (64, 256, 5000, 1 << 16, (1 << 21) + 7, 1 << 24):
+        for frac in (0.5, 0.02):
+            x = rng.standard_normal(n)
+            z = rng.random(n) < frac
+            x[z] = np.where(rng.random(int(z.sum())) < 0.5, 0.0, -0.0)
+            t = _d(x)
+            vx.sort(t)
+            got = _h(t)
+            assert np.array_equal(got, np.sort(x))
+            assert np.array_equal(np.sort(got.view(np.uint64)), np.sort(x.view(np.uint64))), (n, frac)
+    # segments of every length, half zeros of either sign
+    lens = rng.integers(1, 257, size=4000)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    x = rng.standard_normal(int(offs[-1]))
+    z = rng.random(len(x)) < 0.5
+    x[z] = np.where(rng.random(int(z.sum())) < 0.5, 0.0, -0.0)
+    t = _d(x)
+    vx.sort_segments(t, _d(offs))
+    got = _h(t)
+    for s in range(len(lens)):
+        a, b = offs[s], offs[s + 1]
+        assert np.array_equal(got[a:b], np.sort(x[a:b]))
+        assert np.array_equal(np.sort(got[a:b].view(np.uint64)), np.sort(x[a:b].view(np.uint64))), s
